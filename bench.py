@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark: grid-point RK-stage updates/s of the fused WENO5 RHS + SSP-RK3
+stage (BASELINE.json metric) on B200, weak-scaled over radial slabs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--mode mixed|f64] [--nrho 65536] [--ntheta 512]
+
+Workload (config.workload): BASELINE configs[4] shape, 65536 x 512 grid
+points PER GPU (radial slabs of a (65536 N) x 512 grid), extremal-Kerr
+s=-2 m=2 sign structure, WENO5, SSP-RK3, mixed precision (fp32 WENO
+weights, fp64 state) as the headline and fp64 beside it.  Inputs are larger
+than L2 (state 1.07 GB per register, coefficients 2.4 GB), so no explicit
+L2 flush is needed between steps.  Coefficients are synthetic
+(paper_2010_04760_b200/synthetic.py): the reference's own setup would take
+~3.5 min of serial double-double work at this size and is host setup, not
+the measured path.
+
+One JSON line on rank 0.  See DESIGN.md §5 for the roofline bookkeeping.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-point RK-stage updates/s (WENO5 mixed & fp64) at 1/2/4/8 B200, % HBM roofline"
+UNIT = "stage-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t = None
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self):
+        self.marks.append(time.time())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t0, t1 = (self.marks + [0, 0])[:2] if len(self.marks) >= 2 else (0, 1e30)
+        rows = [r for t, r in self.rows if t0 <= t <= t1] or [r for _, r in self.rows]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------- reference arm
+def cpu_reference_rate(seconds: float, nrho=1024, ntheta=512, steps_cap=1000):
+    """The UNMODIFIED reference (oracle/_ref) on all host cores: its own
+    EvolutionRhs + advance_steps in mixed mode (DD state + fp64 weights), RK3,
+    hook off, on a bounded sample grid of the workload's physics.  Returns
+    (updates/s, cores, sample, kind)."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    if O.ref_available():
+        ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22),
+                          nrho, ntheta, mode="mixed", workers=cores)
+        u, lo = ref.initial_data()
+        dt = ref.select_dt()
+        # one step first (also warms the pool), then steps until `seconds`
+        ref.advance(u, lo, dt, 0, 1)
+        done, wall = 0, 0.0
+        (u, lo), st, _ = ref.advance(u, lo, dt, 0, 1)
+        done += 1
+        wall += st["wall_seconds"]
+        per = max(wall, 1e-3)
+        n = max(1, min(steps_cap, int(seconds / per)))
+        (u, lo), st, _ = ref.advance(u, lo, dt, 1, 1 + n)
+        done, wall = n, st["wall_seconds"]
+        rate = nrho * ntheta * 3 * done / wall
+        return rate, cores, f"{nrho}x{ntheta} grid, C5 physics (a=1, s=-2, m=2), reference mixed " \
+                            f"(DD state + fp64 weights), ssprk33, {done} steps, {wall:.1f} s", "reference"
+    # fall back to the C restatement (single thread)
+    from paper_2010_04760_b200 import synthetic
+    prob = synthetic.problem(nrho, ntheta)
+    orc = O.OracleSolver(nrho, ntheta, prob["drho"], prob["dtheta"], prob["parity"],
+                         prob["coef"], prob["cotth"], "weno5", "mixed")
+    u = synthetic.initial_state(prob)
+    t0 = time.time()
+    n = 0
+    while time.time() - t0 < seconds:
+        u, _ = orc.advance(u, synthetic.select_dt(prob), n, n + 1)
+        n += 1
+    wall = time.time() - t0
+    return nrho * ntheta * 3 * n / wall, 1, f"{nrho}x{ntheta} synthetic, C restatement, {n} steps", "port"
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    the unmodified library) on all host cores; one step = one SSP-RK3 step of
+    a bounded 1024x512 sample grid of the workload's physics."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+    cores = os.cpu_count() or 1
+    nrho, ntheta = args.ref_nrho, args.ntheta
+    if not O.ref_available():
+        r, cores, sample, kind = cpu_reference_rate(args.cpu_seconds)
+        v, wall, K = r, 0.0, args.steps
+    else:
+        kind = "reference"
+        ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22),
+                          nrho, ntheta, mode="mixed", workers=cores)
+        u, lo = ref.initial_data()
+        dt = ref.select_dt()
+        (u, lo), _, _ = ref.advance(u, lo, dt, 0, args.warmup)
+        K = args.steps
+        (u, lo), st, _ = ref.advance(u, lo, dt, args.warmup, args.warmup + K)
+        wall = st["wall_seconds"]
+        v = nrho * ntheta * 3 * K / wall
+        sample = (f"{nrho}x{ntheta} grid, C5 physics (a=1, s=-2, m=2), reference mixed "
+                  f"(DD state + fp64 weights), ssprk33, {K} steps, {wall:.1f} s")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": K, "warmup": args.warmup, "ms_per_step": 1000 * wall / max(K, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "dd state, fp64 weights", "data": "synthetic",
+            "config": {"workload": f"C5 physics, bounded CPU sample {nrho}x{ntheta}",
+                       "scheme": "weno5", "stepper": "ssprk33", "mode": "reference mixed"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- B200 arm
+def time_mode(args, mode, prob, world, rank, dev, torch, dist):
+    from paper_2010_04760_b200 import hwgpu, slabs, synthetic
+    spec = hwgpu.SchemeSpec("weno5", mode)
+    g = hwgpu.GpuEvolution(prob["nrho"], prob["ntheta"], prob["drho"], prob["dtheta"],
+                           prob["parity"], prob["coef"], prob["cotth"], spec, device=dev,
+                           rho_offset=prob["rho_offset"], nrho_global=prob["nrho_global"],
+                           coef_ld=prob["nrho"], coef_row0=0)
+    stream = torch.cuda.current_stream()
+    g.set_stream(stream.cuda_stream)
+    u0 = synthetic.initial_state(prob)
+    g.set_state(u0)
+    dt = synthetic.select_dt(prob, "ssprk33")
+    runner = slabs.DistSlab(g, rank, world, "weno5")
+    P = prob["nrho"] * prob["ntheta"]
+    for q in range(args.warmup):
+        runner.step("ssprk33", dt, q)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(3 * K)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    i = 0
+    for q in range(K):
+        for st in range(3):
+            runner.exchange(g.stage_input("ssprk33", st))
+            evs[i][0].record(stream)
+            g.launch_stage("ssprk33", st, dt, args.warmup + q)
+            evs[i][1].record(stream)
+            i += 1
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    total_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    stage_ms = np.array([a.elapsed_time(b) for a, b in evs]).reshape(K, 3)
+    blown, _ = g.status()
+    if blown:
+        raise RuntimeError(f"benchmark state blew up ({mode})")
+    value = world * P * 3 * K / (total_ms / 1000.0)
+    # algorithmic bytes per launch: stage 1 136 B/pt, 2-3 168 B/pt
+    bytes_per_step = P * (136 + 168 + 168)
+    kern_ms = float(stage_ms.sum())
+    achieved = bytes_per_step * K / (kern_ms / 1000.0) / 1e9
+    return g, dict(value=value, total_ms=total_ms, stage_ms=stage_ms, achieved_gbs=achieved,
+                   kern_ms=kern_ms, P=P, dt=dt, u0=u0)
+
+
+def e2e_mode(g, args, prob, world, rank, torch, dist, dt):
+    """Same metric through the C ABI with HOST buffers: per step
+    hwg_set_state (host FieldLayout -> device) + one RK3 step + hwg_get_state."""
+    from paper_2010_04760_b200 import synthetic
+    u = synthetic.initial_state(prob)
+    out = np.zeros_like(u)
+    ke = max(1, min(args.e2e_steps, args.steps))
+    g.set_state(u)
+    g.launch_steps("ssprk33", dt, 0, 1)
+    g.get_state()  # warm the staging buffers
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for q in range(ke):
+        g.set_state(u)
+        g.launch_steps("ssprk33", dt, q, 1)
+        from paper_2010_04760_b200.hwgpu import _lib, _p
+        g._chk(_lib.hwg_get_state(g.h, _p(out)))
+    wall = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([wall], device=f"cuda:{torch.cuda.current_device()}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    P = prob["nrho"] * prob["ntheta"]
+    return dict(value=world * P * 3 * ke / wall, steps=ke,
+                h2d=int(u.nbytes), d2h=int(out.nbytes))
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    from paper_2010_04760_b200 import slabs, synthetic
+
+    ng = args.nrho * world
+    off, cnt = slabs.partition(ng, world)[rank]
+    prob = synthetic.problem(cnt, args.ntheta, rho_offset=off, nrho_global=ng)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    results = {}
+    # headline mode last so its clock window is the one reported
+    modes = ["f64", "mixed"] if args.mode == "mixed" else ["mixed", "f64"]
+    handles = {}
+    for mode in modes:
+        if mode == modes[-1]:
+            clocks.mark()
+        g, r = time_mode(args, mode, prob, world, rank, dev, torch, dist)
+        if mode == modes[-1]:
+            clocks.mark()
+        results[mode] = r
+        handles[mode] = g
+    clocks.stop()
+    head = results[args.mode]
+    g = handles[args.mode]
+    e2e = e2e_mode(g, args, prob, world, rank, torch, dist, head["dt"])
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r, cores, sample, kind = cpu_reference_rate(args.cpu_seconds)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    peak, src = peaks()
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "stage_kernel_traffic.json")
+    if os.path.exists(tf):
+        try:
+            tj = json.load(open(tf))
+            key = f"{args.mode}_{args.nrho}x{args.ntheta}"
+            traffic = tj.get(key)
+        except Exception:
+            traffic = None
+    ach = head["achieved_gbs"]
+    info = g.launch_info()
+    K = args.steps
+    line = {
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": head["total_ms"] / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 state, fp32 WENO weights" if args.mode == "mixed" else "f64",
+        "data": "synthetic (BASELINE shape; synthetic coefficient planes, Gaussian pulse)",
+        "config": {"workload": f"C5 shape {args.nrho}x{args.ntheta} per GPU (radial slabs of "
+                               f"{args.nrho * world}x{args.ntheta}), WENO5 {args.mode}, SSP-RK3",
+                   "grid_points_per_gpu": head["P"], "stages_per_step": 3,
+                   "l2": "inputs larger than L2 (no flush needed)",
+                   "parallelism": f"rho-slabs x{world}"},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": traffic, "peak_source": src,
+                     "kernel": "hwg::stage_kernel<WENO5>",
+                     "bytes_per_point_stage": 157.33},
+        "clocks": clocks.summary(),
+        "e2e": {"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
+                "d2h_bytes_per_step": e2e["d2h"], "steps": e2e["steps"],
+                "path": "C ABI hwg_set_state + 1 RK3 step + hwg_get_state (host FieldLayout fp64)"},
+        "gpu_launches": 3 * K,
+        "launch": info,
+        "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / K,
+                      "stage_kernel_gbs": r["achieved_gbs"], "frac": r["achieved_gbs"] / peak,
+                      "stage_ms_mean": [float(x) for x in r["stage_ms"].mean(axis=0)]}
+                  for m, r in results.items()},
+        "mixed_vs_fp64_speedup": results["mixed"]["value"] / results["f64"]["value"],
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--mode", default="mixed", choices=["mixed", "f64"])
+    ap.add_argument("--nrho", type=int, default=65536)
+    ap.add_argument("--ntheta", type=int, default=512)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-nrho", type=int, default=1024)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

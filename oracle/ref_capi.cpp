@@ -1,0 +1,331 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// A flat C ABI over the *unmodified* reference library (libhweno built from
+// /root/reference/proj/src by oracle/Makefile).  It lets the Python tests and
+// bench.py's cpu_baseline / --impl reference leg drive the reference's own
+// setup and hot path:
+//   make_grid / assemble_coefficients      proj/src/geometry.cpp:73-168
+//   EvolutionRhs (ctor, operator())        proj/src/evolve.cpp:10-187
+//   initial_data                           proj/src/evolve.cpp:189-215
+//   select_dt / stepper_step               proj/include/hweno/timestep.hpp:25-118
+//   advance_steps                          proj/src/evolve.cpp:237-265
+//   HorizonSampler / multipole_project     proj/src/diagnostics.cpp:128-283
+// No reference source is copied here; only its public headers are included.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "hweno/angular.hpp"
+#include "hweno/diagnostics.hpp"
+#include "hweno/evolve.hpp"
+#include "hweno/geometry.hpp"
+#include "hweno/parallel.hpp"
+#include "hweno/timestep.hpp"
+
+using namespace hweno;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct RefHandle {
+  PhysicalParams p;
+  Grid g;
+  CoefficientSet cs;
+  SchemeSpec spec;
+  std::unique_ptr<WorkerPool> pool;
+  std::unique_ptr<EvolutionRhs> rhs;
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+void to_dd(const StateVec& u, double* out) {
+  for (size_t i = 0; i < u.size(); ++i) {
+    out[2 * i] = u[i].hi;
+    out[2 * i + 1] = u[i].lo;
+  }
+}
+
+StateVec from_dd(const double* in, size_t n) {
+  StateVec u(n);
+  for (size_t i = 0; i < n; ++i) u[i] = DDReal(in[2 * i], in[2 * i + 1]);
+  return u;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// scheme: 0 weno5, 1 weno3, 2 fd6ko; mode: 0 full (DD weights), 1 mixed
+// (fp64 weights).  eps may be +inf (frozen linear weights).
+int ref_create(double M, double a, int spin, int mmode, double S, int nrho,
+               int ntheta, int scheme, int mode, double eps, double sigma,
+               int workers, void** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto h = std::make_unique<RefHandle>();
+    h->p.M = WorkReal(M);
+    h->p.a = WorkReal(a);
+    h->p.spin = spin;
+    h->p.mmode = mmode;
+    h->p.S = WorkReal(S);
+    h->g = make_grid(nrho, ntheta, h->p);
+    h->cs = assemble_coefficients(h->g, h->p);
+    h->spec.scheme = scheme == 0 ? Scheme::weno5
+                     : scheme == 1 ? Scheme::weno3
+                                   : Scheme::fd6ko;
+    h->spec.mode = mode == 0 ? PrecisionMode::full : PrecisionMode::mixed;
+    h->spec.eps = WorkReal(eps);
+    h->spec.sigma = WorkReal(sigma);
+    h->pool = std::make_unique<WorkerPool>(workers);
+    h->rhs = std::make_unique<EvolutionRhs>(h->g, h->cs, h->p, h->spec,
+                                            *h->pool);
+    *out = h.release();
+  });
+}
+
+void ref_destroy(void* hv) { delete static_cast<RefHandle*>(hv); }
+
+// dbl[0..] = drho, dtheta, rho_min, max_speed, horizon_rho, S  (hi parts)
+// dlo[..]  = the matching lo parts
+// ints[0..] = nrho, ntheta, parity, horizon_index, state_size
+int ref_info(void* hv, double* dbl, double* dlo, long long* ints) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    WorkReal v[6] = {h->g.drho, h->g.dtheta, h->g.rho_min, h->cs.max_speed,
+                     horizon_rho(h->p), h->p.S};
+    for (int i = 0; i < 6; ++i) {
+      dbl[i] = v[i].hi;
+      if (dlo) dlo[i] = v[i].lo;
+    }
+    ints[0] = h->g.nrho;
+    ints[1] = h->g.ntheta;
+    ints[2] = ((h->p.mmode + h->p.spin) % 2 == 0) ? 1 : -1;
+    ints[3] = h->g.horizon_index;
+    ints[4] = (long long)h->rhs->layout().size();
+  });
+}
+
+// planes: 9*P doubles in the order b, lam, w_re, w_im, bt_re, bt_im, c_re,
+// c_im, ath, each indexed j + nrho*k (the reference's CoefficientSet order).
+// lo (optional) receives the low limbs.  cotth: ntheta.  rho/theta: grids.
+int ref_coeffs(void* hv, double* planes, double* lo, double* cotth,
+               double* rho, double* theta) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    const std::vector<WorkReal>* src[9] = {
+        &h->cs.b,     &h->cs.lam,   &h->cs.w_re, &h->cs.w_im, &h->cs.bt_re,
+        &h->cs.bt_im, &h->cs.c_re,  &h->cs.c_im, &h->cs.ath};
+    size_t P = size_t(h->g.nrho) * h->g.ntheta;
+    for (int q = 0; q < 9; ++q)
+      for (size_t i = 0; i < P; ++i) {
+        planes[q * P + i] = (*src[q])[i].hi;
+        if (lo) lo[q * P + i] = (*src[q])[i].lo;
+      }
+    if (cotth)
+      for (int k = 0; k < h->g.ntheta; ++k) cotth[k] = h->cs.cotth[k].hi;
+    if (rho)
+      for (int j = 0; j < h->g.nrho; ++j) rho[j] = h->g.rho[j].hi;
+    if (theta)
+      for (int k = 0; k < h->g.ntheta; ++k) theta[k] = h->g.theta[k].hi;
+  });
+}
+
+// u_dd: 2*state_size doubles ({hi, lo} pairs, reference FieldLayout)
+int ref_initial_data(void* hv, int ell, double center, double width,
+                     double amplitude, double* u_dd) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    InitialDataSpec id;
+    id.ell = ell;
+    id.center = WorkReal(center);
+    id.width = WorkReal(width);
+    id.amplitude = WorkReal(amplitude);
+    to_dd(initial_data(h->g, h->cs, h->p, id), u_dd);
+  });
+}
+
+// EvolutionRhs::operator(): u_dd's ghosts are filled in place, du_dd gets
+// the interior RHS (its ghosts are zeroed).
+int ref_rhs(void* hv, double* u_dd, double* du_dd) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    size_t n = h->rhs->layout().size();
+    StateVec u = from_dd(u_dd, n);
+    StateVec du(n);
+    (*h->rhs)(u, du);
+    to_dd(u, u_dd);
+    to_dd(du, du_dd);
+  });
+}
+
+int ref_apply_boundaries(void* hv, double* u_dd) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    size_t n = h->rhs->layout().size();
+    StateVec u = from_dd(u_dd, n);
+    h->rhs->apply_boundaries(u);
+    to_dd(u, u_dd);
+  });
+}
+
+// stepper: 0 ssprk33, 1 ssprk104
+int ref_select_dt(void* hv, int stepper, double cfl, double* dt_dd) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    StepperSpec st;
+    st.kind = stepper == 0 ? StepperSpec::ssprk33 : StepperSpec::ssprk104;
+    st.cfl = WorkReal(cfl);
+    WorkReal dt = select_dt(h->g, h->cs, st);
+    dt_dd[0] = dt.hi;
+    dt_dd[1] = dt.lo;
+  });
+}
+
+// advance_steps with the hook disabled, or (ktheta >= 0) with a hook that
+// records the HorizonSampler observables (phi, dphi1..3; re, im each: 8
+// doubles hi) plus tau.hi per sample into obs (capacity max_obs rows of 9).
+// stats: steps_done, blew_up, blowup_step, n_obs; wall seconds in *wall.
+int ref_advance(void* hv, int stepper, double cfl, const double* dt_dd,
+                long s0, long s1, double* u_dd, long hook_every, int ktheta,
+                double* obs, long max_obs, long* stats, double* wall) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    StepperSpec st;
+    st.kind = stepper == 0 ? StepperSpec::ssprk33 : StepperSpec::ssprk104;
+    st.cfl = WorkReal(cfl);
+    size_t n = h->rhs->layout().size();
+    StateVec u = from_dd(u_dd, n);
+    WorkReal dt(dt_dd[0], dt_dd[1]);
+    SampleHook hook;
+    long n_obs = 0;
+    std::unique_ptr<HorizonSampler> hs;
+    if (ktheta >= 0) {
+      hs = std::make_unique<HorizonSampler>(h->g, h->p, h->rhs->layout(),
+                                            ktheta);
+      hook.every = hook_every;
+      hook.fn = [&](long, const WorkReal& tau, const StateVec& s) {
+        if (n_obs >= max_obs) return;
+        HorizonObservables ob = hs->sample(s);
+        double* row = obs + 9 * n_obs;
+        row[0] = tau.hi;
+        row[1] = ob.phi.re.hi;
+        row[2] = ob.phi.im.hi;
+        for (int d = 0; d < 3; ++d) {
+          row[3 + 2 * d] = ob.dphi[d].re.hi;
+          row[4 + 2 * d] = ob.dphi[d].im.hi;
+        }
+        ++n_obs;
+      };
+    }
+    RunStats rs =
+        advance_steps(*h->rhs, st, u, dt, s0, s1, hook, *h->pool);
+    to_dd(u, u_dd);
+    stats[0] = rs.steps_done;
+    stats[1] = rs.blew_up ? 1 : 0;
+    stats[2] = rs.blowup_step;
+    stats[3] = n_obs;
+    if (wall) *wall = rs.wall_seconds;
+  });
+}
+
+// HorizonSampler weights for row ktheta, extracted through the sampler's
+// public sample() with unit states (so they are exactly the reference's):
+// w[d*8 + i] multiplies Psi(j0 + i) for derivative order d (widths 5..8;
+// unused tail entries are 0).  *j0 = base index.
+int ref_horizon_weights(void* hv, int ktheta, int* j0, double* w) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    const FieldLayout& lay = h->rhs->layout();
+    HorizonSampler hs(h->g, h->p, lay, ktheta);
+    *j0 = hs.base_index();
+    StateVec u(lay.size());
+    for (int i = 0; i < 8; ++i) {
+      std::fill(u.begin(), u.end(), WorkReal(0));
+      u[lay.at(0, *j0 + i, ktheta)] = WorkReal(1);
+      HorizonObservables ob = hs.sample(u);
+      w[0 * 8 + i] = ob.phi.re.hi;
+      for (int d = 0; d < 3; ++d) w[(d + 1) * 8 + i] = ob.dphi[d].re.hi;
+    }
+  });
+}
+
+// Linear weights of multipole_project over a staggered theta slice of
+// length ntheta (projection of the unit slices e_k).
+int ref_projection_weights(int ntheta, int spin, int mmode, int ell,
+                           double* w) {
+  return guarded([&] {
+    std::vector<WorkReal> slice(ntheta);
+    for (int k = 0; k < ntheta; ++k) {
+      std::fill(slice.begin(), slice.end(), WorkReal(0));
+      slice[k] = WorkReal(1);
+      w[k] = multipole_project(slice, spin, mmode, ell).hi;
+    }
+  });
+}
+
+int ref_multipole_project(const double* slice_hi, int ntheta, int spin,
+                          int mmode, int ell, double* out) {
+  return guarded([&] {
+    std::vector<WorkReal> slice(ntheta);
+    for (int k = 0; k < ntheta; ++k) slice[k] = WorkReal(slice_hi[k]);
+    *out = multipole_project(slice, spin, mmode, ell).hi;
+  });
+}
+
+// Row-level stencil KATs (proj/include/hweno/spatial.hpp): one weno5 row
+// derivative in full (mode 0) or mixed (mode 1) precision.  u_dd holds
+// n + 8 values (4 ghosts each side).
+int ref_weno5_row(const double* u_dd, int n, double drho, double eps,
+                  int mode, int minus, double* du_dd) {
+  return guarded([&] {
+    StateVec u = from_dd(u_dd, size_t(n) + 8);
+    StateVec du(n);
+    if (mode == 0)
+      weno5_row_derivative<WorkReal>(u.data() + 4, n, WorkReal(drho),
+                                     WorkReal(eps), minus != 0, du.data());
+    else
+      weno5_row_derivative<WeightReal>(u.data() + 4, n, WorkReal(drho), eps,
+                                       minus != 0, du.data());
+    to_dd(du, du_dd);
+  });
+}
+
+// weno5 weights (proj/include/hweno/spatial.hpp:29-65), mode 0 DD / 1 fp64
+int ref_weno5_weights(const double* a5, double eps, int mode, double* w3) {
+  return guarded([&] {
+    WorkReal a[5];
+    for (int i = 0; i < 5; ++i) a[i] = WorkReal(a5[i]);
+    if (mode == 0) {
+      WorkReal w[3];
+      weno5_weights_t<WorkReal>(a[0], a[1], a[2], a[3], a[4], WorkReal(eps),
+                                w);
+      for (int i = 0; i < 3; ++i) w3[i] = w[i].hi;
+    } else {
+      double w[3];
+      weno5_weights_t<WeightReal>(a[0], a[1], a[2], a[3], a[4], eps, w);
+      for (int i = 0; i < 3; ++i) w3[i] = w[i];
+    }
+  });
+}
+
+int ref_nthreads_hint(void) { return (int)std::thread::hardware_concurrency(); }
+
+}  // extern "C"

@@ -1,0 +1,294 @@
+"""ctypes binding of libhwgpu.so (include/hweno_gpu.h) and a thin Python
+mirror of the reference's hot-path interface:
+
+    GpuEvolution(...)            ~ hweno::EvolutionRhs   (proj/include/hweno/evolve.hpp:56-82)
+    GpuEvolution.rhs(u)          ~ EvolutionRhs::operator()(u, du)
+    GpuEvolution.advance(...)    ~ hweno::advance_steps  (proj/src/evolve.cpp:237-265)
+
+States on the host use the reference FieldLayout as numpy arrays of shape
+(4, ntheta + 4, nrho + 8) (component, theta row incl. 2 ghosts, rho column
+incl. 4 ghosts).  There is no CPU fallback: importing this module without
+the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .build import SO
+
+if not os.path.exists(SO):
+    raise ImportError(f"libhwgpu.so not built ({SO}); run python -m paper_2010_04760_b200.build")
+
+_lib = C.CDLL(SO)
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+SCHEMES = {"weno5": 0, "weno3": 1, "fd6ko": 2}
+PRECISIONS = {"f64": 0, "mixed": 1}
+STEPPERS = {"ssprk33": 0, "ssprk104": 1}
+STAGES = {"ssprk33": 3, "ssprk104": 10}
+HALO = 4
+
+
+class HwgDesc(C.Structure):
+    _fields_ = [("nrho", C.c_int), ("ntheta", C.c_int), ("drho", C.c_double),
+                ("dtheta", C.c_double), ("parity", C.c_int), ("scheme", C.c_int),
+                ("precision", C.c_int), ("eps", C.c_double), ("sigma", C.c_double),
+                ("device", C.c_int), ("rho_offset", C.c_int), ("nrho_global", C.c_int),
+                ("coef_ld", C.c_int), ("coef_row0", C.c_int)]
+
+
+class HwgRunStats(C.Structure):
+    _fields_ = [("steps_done", C.c_longlong), ("wall_seconds", C.c_double),
+                ("blew_up", C.c_int), ("blowup_step", C.c_longlong)]
+
+
+class HwgObservables(C.Structure):
+    _fields_ = [("phi", C.c_double * 2), ("dphi", (C.c_double * 2) * 3), ("obs", C.c_double * 2),
+                ("scri", C.c_double * 2), ("proj", C.c_double * 2)]
+
+    def as_dict(self):
+        return dict(phi=complex(*self.phi), dphi=[complex(*d) for d in self.dphi],
+                    obs=complex(*self.obs), scri=complex(*self.scri),
+                    proj=complex(*self.proj))
+
+
+HOOK = C.CFUNCTYPE(None, C.c_longlong, C.c_double, C.c_double, C.POINTER(HwgObservables), C.c_void_p)
+
+_lib.hwg_last_error.restype = C.c_char_p
+_lib.hwg_last_error.argtypes = [_vp]
+_lib.hwg_create.argtypes = [C.POINTER(HwgDesc), _dp, _dp, C.POINTER(_vp)]
+_lib.hwg_destroy.argtypes = [_vp]
+_lib.hwg_set_stream.argtypes = [_vp, _vp]
+for _f in ("hwg_set_state_dd", "hwg_get_state_dd", "hwg_set_state", "hwg_get_state"):
+    getattr(_lib, _f).argtypes = [_vp, _dp]
+_lib.hwg_rhs.argtypes = [_vp, _dp, _dp]
+_lib.hwg_rhs_dd.argtypes = [_vp, _dp, _dp]
+_lib.hwg_advance.argtypes = [_vp, C.c_int, C.c_double, C.c_double, C.c_longlong, C.c_longlong,
+                             C.c_longlong, HOOK, _vp, C.POINTER(HwgRunStats)]
+_lib.hwg_set_observers.argtypes = [_vp, C.c_int, C.c_int, _dp, C.c_int, _dp]
+_lib.hwg_observe.argtypes = [_vp, C.POINTER(HwgObservables)]
+_lib.hwg_launch_stage.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_longlong]
+_lib.hwg_launch_steps.argtypes = [_vp, C.c_int, C.c_double, C.c_double, C.c_longlong, C.c_longlong]
+_lib.hwg_stage_input.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(C.c_int)]
+_lib.hwg_register_planes.argtypes = [_vp, C.c_int, C.POINTER(_vp), C.POINTER(_vp),
+                                     C.POINTER(C.c_int)]
+_lib.hwg_current_register.argtypes = [_vp]
+_lib.hwg_status.argtypes = [_vp, C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.c_int]
+_lib.hwg_launch_info.argtypes = [_vp] + [C.POINTER(C.c_int)] * 5
+_lib.hwg_synchronize.argtypes = [_vp]
+
+EXPORTED = ["hwg_create", "hwg_destroy", "hwg_last_error", "hwg_set_stream", "hwg_set_state_dd",
+            "hwg_get_state_dd", "hwg_set_state", "hwg_get_state", "hwg_rhs", "hwg_rhs_dd",
+            "hwg_advance", "hwg_set_observers", "hwg_observe", "hwg_launch_stage",
+            "hwg_launch_steps", "hwg_stage_input", "hwg_register_planes",
+            "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize"]
+
+
+class HwgError(RuntimeError):
+    pass
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+@dataclass
+class SchemeSpec:
+    """SchemeSpec (proj/include/hweno/evolve.hpp:37-42); mode is the GPU tier
+    ('f64' ~ reference full, 'mixed' ~ reference mixed)."""
+    scheme: str = "weno5"
+    mode: str = "mixed"
+    eps: float = 1e-6
+    sigma: float = 0.01
+
+
+class _DevArray:
+    """Zero-copy __cuda_array_interface__ view of a device pointer (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, shape, typestr="<f8"):
+        self.__cuda_array_interface__ = dict(shape=tuple(shape), typestr=typestr,
+                                             data=(int(ptr), False), version=3, strides=None)
+
+
+class GpuEvolution:
+    """One handle = one GPU (or one radial slab of the grid)."""
+
+    def __init__(self, nrho: int, ntheta: int, drho: float, dtheta: float, parity: int,
+                 coef: np.ndarray, cotth: np.ndarray, spec: SchemeSpec = SchemeSpec(),
+                 device: int = 0, rho_offset: int = 0, nrho_global: int | None = None,
+                 coef_ld: int = 0, coef_row0: int = -1):
+        self._coef = np.ascontiguousarray(coef, dtype=np.float64).ravel()
+        self._cot = np.ascontiguousarray(cotth, dtype=np.float64)
+        d = HwgDesc(nrho, ntheta, drho, dtheta, parity, SCHEMES[spec.scheme],
+                    PRECISIONS[spec.mode], spec.eps, spec.sigma, device, rho_offset,
+                    nrho_global or nrho, coef_ld, coef_row0)
+        h = _vp()
+        rc = _lib.hwg_create(C.byref(d), _p(self._coef), _p(self._cot), C.byref(h))
+        if rc != 0:
+            msg = _lib.hwg_last_error(None).decode()
+            if rc == 2:
+                raise ValueError(msg)
+            raise HwgError(msg)
+        self.h = h
+        self._coef = None  # host copy no longer needed
+        self.nrho, self.ntheta, self.spec, self.parity = nrho, ntheta, spec, parity
+        self.drho, self.dtheta = drho, dtheta
+
+    @classmethod
+    def from_reference(cls, ref, spec: SchemeSpec | None = None, device: int = 0):
+        """From a reference handle (oracle.RefSolver) — used by tests only."""
+        spec = spec or SchemeSpec(ref.scheme, "f64" if ref.mode == "full" else "mixed",
+                                  ref.eps, ref.sigma)
+        return cls(ref.nrho, ref.ntheta, ref.drho, ref.dtheta, ref.parity, ref.coef, ref.cotth,
+                   spec, device)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.hwg_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # ------------------------------------------------------------------ util
+    def _chk(self, rc):
+        if rc != 0:
+            msg = _lib.hwg_last_error(self.h).decode()
+            if rc == 2:
+                raise ValueError(msg)
+            raise HwgError(msg)
+
+    @property
+    def shape(self):
+        return (4, self.ntheta + 4, self.nrho + 8)
+
+    def set_stream(self, stream_ptr: int | None):
+        self._chk(_lib.hwg_set_stream(self.h, _vp(stream_ptr or 0)))
+
+    # ------------------------------------------------------------------ state
+    def set_state(self, u: np.ndarray, lo: np.ndarray | None = None):
+        if lo is not None:
+            dd = np.empty(u.size * 2)
+            dd[0::2] = u.ravel()
+            dd[1::2] = lo.ravel()
+            self._chk(_lib.hwg_set_state_dd(self.h, _p(dd)))
+        else:
+            self._chk(_lib.hwg_set_state(self.h, _p(np.ascontiguousarray(u, dtype=np.float64))))
+
+    def get_state(self) -> np.ndarray:
+        u = np.zeros(self.shape)
+        self._chk(_lib.hwg_get_state(self.h, _p(u)))
+        return u
+
+    def get_state_dd(self):
+        dd = np.zeros(2 * int(np.prod(self.shape)))
+        self._chk(_lib.hwg_get_state_dd(self.h, _p(dd)))
+        return dd[0::2].reshape(self.shape).copy(), dd[1::2].reshape(self.shape).copy()
+
+    # ------------------------------------------------------------------ rhs
+    def rhs(self, u: np.ndarray, du: np.ndarray | None = None):
+        """EvolutionRhs::operator(): returns (u with ghosts filled, du)."""
+        u = np.ascontiguousarray(u, dtype=np.float64).copy()
+        du = np.zeros(self.shape) if du is None else np.ascontiguousarray(du).copy()
+        self._chk(_lib.hwg_rhs(self.h, _p(u), _p(du)))
+        return u, du
+
+    # ------------------------------------------------------------------ loop
+    def advance(self, stepper: str, dt, step_begin: int, step_end: int, every: int = 1,
+                hook=None):
+        """advance_steps: hook(step, (tau_hi, tau_lo), observables dict)."""
+        dt_hi, dt_lo = (dt if isinstance(dt, tuple) else (float(dt), 0.0))
+        stats = HwgRunStats()
+        errors = []
+
+        def _cb(step, thi, tlo, obs, user):
+            try:
+                hook(int(step), (thi, tlo), obs.contents.as_dict())
+            except Exception as e:  # noqa: BLE001 - re-raised below
+                errors.append(e)
+
+        cb = HOOK(_cb) if hook is not None else HOOK()
+        self._chk(_lib.hwg_advance(self.h, STEPPERS[stepper], dt_hi, dt_lo, step_begin, step_end,
+                                   every, cb, None, C.byref(stats)))
+        if errors:
+            raise errors[0]
+        return dict(steps_done=stats.steps_done, wall_seconds=stats.wall_seconds,
+                    blew_up=bool(stats.blew_up), blowup_step=stats.blowup_step)
+
+    def set_observers(self, kobs: int, j0: int, hweights, jobs: int, pweights):
+        hw = None if hweights is None else np.ascontiguousarray(hweights, dtype=np.float64).ravel()
+        pw = None if pweights is None else np.ascontiguousarray(pweights, dtype=np.float64)
+        self._chk(_lib.hwg_set_observers(self.h, kobs, j0, _p(hw) if hw is not None else None,
+                                         jobs, _p(pw) if pw is not None else None))
+
+    def observe(self) -> dict:
+        o = HwgObservables()
+        self._chk(_lib.hwg_observe(self.h, C.byref(o)))
+        return o.as_dict()
+
+    # ------------------------------------------------------------------ device level
+    def launch_stage(self, stepper: str, stage: int, dt, step: int):
+        dt_hi, dt_lo = (dt if isinstance(dt, tuple) else (float(dt), 0.0))
+        self._chk(_lib.hwg_launch_stage(self.h, STEPPERS[stepper], stage, dt_hi, dt_lo, step))
+
+    def launch_steps(self, stepper: str, dt, step_begin: int, nsteps: int):
+        dt_hi, dt_lo = (dt if isinstance(dt, tuple) else (float(dt), 0.0))
+        self._chk(_lib.hwg_launch_steps(self.h, STEPPERS[stepper], dt_hi, dt_lo, step_begin,
+                                        nsteps))
+
+    def stage_input(self, stepper: str, stage: int) -> int:
+        r = C.c_int()
+        self._chk(_lib.hwg_stage_input(self.h, STEPPERS[stepper], stage, C.byref(r)))
+        return r.value
+
+    def current_register(self) -> int:
+        return _lib.hwg_current_register(self.h)
+
+    def register_planes(self, reg: int):
+        """(psi_row0_ptr, pi_row0_ptr, row_pitch) of a state register."""
+        a, b, p = _vp(), _vp(), C.c_int()
+        self._chk(_lib.hwg_register_planes(self.h, reg, C.byref(a), C.byref(b), C.byref(p)))
+        return a.value, b.value, p.value
+
+    def register_views(self, reg: int):
+        """torch views (rows -4..nrho+3, pitch, 2) of a register's psi and pi planes."""
+        import torch
+        ps, pi, pitch = self.register_planes(reg)
+        rows = self.nrho + 2 * HALO
+        off = HALO * pitch * 16
+        views = []
+        for ptr in (ps, pi):
+            t = torch.as_tensor(_DevArray(ptr - off, (rows, pitch, 2)), device="cuda")
+            views.append(t)
+        return views
+
+    def status(self, clear: bool = False):
+        b, s = C.c_int(), C.c_longlong()
+        self._chk(_lib.hwg_status(self.h, C.byref(b), C.byref(s), int(clear)))
+        return bool(b.value), s.value
+
+    def launch_info(self):
+        v = [C.c_int() for _ in range(5)]
+        self._chk(_lib.hwg_launch_info(self.h, *[C.byref(x) for x in v]))
+        return dict(zip(("blocks", "threads", "nranges", "nchunks", "pitch"), (x.value for x in v)))
+
+    def synchronize(self):
+        self._chk(_lib.hwg_synchronize(self.h))
+
+
+def stage_bytes(stepper: str) -> float:
+    """Algorithmic HBM bytes per grid point per stage:
+    fp64 state 32 B per register touched + 9 fp64 coefficient planes (72 B)."""
+    if stepper == "ssprk33":
+        return (136 + 168 + 168) / 3.0
+    return 1520 / 10.0
+
+
+def dd_div(a: float, b: float) -> float:
+    return a / b if math.isfinite(a) else a

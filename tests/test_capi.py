@@ -1,0 +1,70 @@
+"""CPU tests of the C ABI: the library builds for sm_100a, loads, and exports
+every entry point include/hweno_gpu.h declares (no compute without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "hweno_gpu.h")
+
+
+def declared():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(hwg_[a-z_0-9]+)\s*\(", txt)) - {"hwg_hook_fn"})
+
+
+def test_header_declares_entry_points():
+    names = declared()
+    for must in ("hwg_create", "hwg_rhs", "hwg_advance", "hwg_set_state_dd", "hwg_get_state_dd",
+                 "hwg_destroy", "hwg_last_error", "hwg_observe", "hwg_set_observers"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2010_04760_b200.build import SO, build_cuda
+    build_cuda()
+    lib = ctypes.CDLL(SO)
+    for name in declared():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", SO], capture_output=True, text=True).stdout
+    for name in declared():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_binding_lists_every_symbol():
+    from paper_2010_04760_b200 import hwgpu
+    assert sorted(hwgpu.EXPORTED) == declared()
+
+
+def test_library_is_sm100a():
+    from paper_2010_04760_b200.build import SO
+    out = subprocess.run(["cuobjdump", "--list-elf", SO], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_create_without_gpu_fails_loudly():
+    """No CPU fallback: on a box without a GPU the handle cannot be created."""
+    import numpy as np
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, HwgError
+    with pytest.raises(HwgError):
+        GpuEvolution(16, 4, 0.1, 0.5, 1, np.zeros(9 * 64), np.zeros(4))
+
+
+def test_create_validates_like_the_reference():
+    """EvolutionRhs ctor errors (evolve.cpp:16-17, 26-28) surface before any
+    device work: invalid_argument -> ValueError, runtime_error -> HwgError."""
+    import numpy as np
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, HwgError
+    with pytest.raises(ValueError):
+        GpuEvolution(8, 4, 0.1, 0.5, 1, np.zeros(9 * 32), np.zeros(4))
+    coef = np.zeros((9, 4, 16))
+    coef[1, 0, :] = -1.0
+    coef[1, 0, 5] = 1.0  # lam: - - - - - + - - ... changes sign twice
+    with pytest.raises(HwgError, match="more than once"):
+        GpuEvolution(16, 4, 0.1, 0.5, 1, coef, np.zeros(4))

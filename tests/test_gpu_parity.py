@@ -1,0 +1,202 @@
+"""GPU parity tests: the CUDA hot path through the C ABI against the oracle
+(C restatement) and the golden vectors of the unmodified reference library.
+
+Tolerances (normwise relative L-inf over the interior):
+  * one RHS, GPU fp64 vs reference full (DD) / vs fp64 oracle: 1e-13
+    (different fp64 rounding only: FMA contraction, one reciprocal per WENO
+    interface instead of five divisions)
+  * one RHS, GPU mixed (fp32 weights) vs reference mixed (DD + fp64 weights): 1e-6
+  * evolution: fp64 vs reference full 1e-12; mixed vs reference mixed 1e-6
+    (BASELINE.json north_star)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_cases, load_golden
+from helpers import gpu_from_golden, interior, oracle_from_golden, rel_linf
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_rhs_fp64_matches_reference_and_oracle(cuda_ok, case):
+    g = load_golden(case)
+    gpu = gpu_from_golden(g, "f64")
+    orc = oracle_from_golden(g, "f64")
+    for u, key in ((g["u0"], "rhs_full"), (g["urand"], "rhs_rand_full")):
+        ug, du = gpu.rhs(u)
+        uo, duo = orc.rhs(u)
+        assert rel_linf(du, g[key]) <= 1e-13, key
+        assert rel_linf(du, duo) <= 1e-13, key
+        # ghosts of u are filled in place exactly as the reference does
+        assert np.array_equal(ug, uo)
+        # du ghost entries are never touched
+        assert np.all(du[:, :2, :] == 0) and np.all(du[:, :, :4] == 0)
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_rhs_mixed_matches_reference_mixed(cuda_ok, case):
+    g = load_golden(case)
+    gpu = gpu_from_golden(g, "mixed")
+    orc = oracle_from_golden(g, "mixed")
+    for u, key in ((g["u0"], "rhs_mixed"), (g["urand"], "rhs_rand_mixed")):
+        _, du = gpu.rhs(u)
+        _, duo = orc.rhs(u)
+        assert rel_linf(du, g[key]) <= 1e-6, key
+        assert rel_linf(du, duo) <= 1e-6, key
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_rhs_frozen_weights_linear(cuda_ok, case):
+    """eps = inf (spatial.hpp:15-18): linear reconstruction; matches the
+    reference's linear RHS and is linear (test_evolve.cpp:172-225)."""
+    g = load_golden(case)
+    for mode in ("f64", "mixed"):
+        gpu = gpu_from_golden(g, mode, eps=math.inf)
+        _, du = gpu.rhs(g["urand"])
+        assert rel_linf(du, g["rhs_rand_linear"]) <= (1e-13 if mode == "f64" else 1e-6)
+    gpu = gpu_from_golden(g, "f64", eps=math.inf)
+    rng = np.random.default_rng(3)
+    v = np.zeros_like(g["urand"])
+    v[:, 2:-2, 4:-4] = rng.uniform(-1, 1, interior(v).shape)
+    al, be = 7 / 16, -19 / 8
+    _, fu = gpu.rhs(g["urand"])
+    _, fv = gpu.rhs(v)
+    _, fw = gpu.rhs(al * g["urand"] + be * v)
+    assert rel_linf(fw, al * fu + be * fv) <= 1e-13
+
+
+@pytest.mark.parametrize("scheme", ["weno5", "weno3", "fd6ko"])
+@pytest.mark.parametrize("mode", ["f64", "mixed"])
+def test_zero_state_zero_rhs(cuda_ok, scheme, mode):
+    g = load_golden("extremal_w5")
+    gpu = gpu_from_golden(g, mode, scheme=scheme)
+    _, du = gpu.rhs(np.zeros(gpu.shape))
+    assert np.all(du == 0.0)
+
+
+@pytest.mark.parametrize("case", golden_cases())
+def test_evolution_matches_reference(cuda_ok, case):
+    g = load_golden(case)
+    dt = (float(g["dt"][0]), float(g["dt"][1]))
+    for mode, key, tol in (("f64", "state_full", 1e-12), ("mixed", "state_mixed", 1e-6)):
+        gpu = gpu_from_golden(g, mode)
+        gpu.set_state(g["u0"])
+        st = gpu.advance(str(g["stepper"]), dt, 0, int(g["steps"]))
+        assert not st["blew_up"] and st["steps_done"] == int(g["steps"])
+        u = gpu.get_state()
+        assert rel_linf(u, g[key]) <= tol, (mode, rel_linf(u, g[key]))
+
+
+def test_hook_cadence_and_restart(cuda_ok):
+    """proj/tests/test_evolve.cpp:321-350."""
+    g = load_golden("extremal_w5")
+    gpu = gpu_from_golden(g, "mixed")
+    gpu.set_state(g["u0"])
+    dt = (float(g["dt"][0]), float(g["dt"][1]))
+    seen = []
+    st = gpu.advance("ssprk33", dt, 0, 10, every=4, hook=lambda s, tau, ob: seen.append((s, tau)))
+    assert st["steps_done"] == 10 and not st["blew_up"]
+    assert [s for s, _ in seen] == [0, 4, 8, 10]
+    for s, tau in seen:
+        assert abs(tau[0] - s * dt[0]) <= 1e-15 * max(1, s)
+    seen.clear()
+    st = gpu.advance("ssprk33", dt, 10, 14, every=4, hook=lambda s, tau, ob: seen.append(s))
+    assert st["steps_done"] == 4 and seen == [10, 12, 14]
+
+
+def test_blowup_freezes_state(cuda_ok):
+    """proj/tests/test_evolve.cpp:352-361 and evolve.cpp:253-258."""
+    g = load_golden("extremal_w5")
+    gpu = gpu_from_golden(g, "mixed")
+    u = g["u0"].copy()
+    u[0, 2 + 1, 4 + 30] = 1e31
+    gpu.set_state(u)
+    dt = (float(g["dt"][0]), float(g["dt"][1]))
+    seen = []
+    st = gpu.advance("ssprk33", dt, 0, 5, every=1, hook=lambda s, tau, ob: seen.append(s))
+    assert st["blew_up"] and st["blowup_step"] == 1 and st["steps_done"] == 1
+    assert seen == [0]
+    frozen = gpu.get_state()
+    orc = oracle_from_golden(g, "mixed")
+    uo, _ = orc.advance(u, dt[0], 0, 5)
+    assert rel_linf(frozen, uo) <= 1e-6
+
+
+def test_observers_match_reference(cuda_ok):
+    import oracle as O
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=0), 128, 8, mode="mixed")
+    u, ulo = ref.initial_data(O.Physics(a=1.0, spin=-2, mmode=0, center=3.0, width=0.5))
+    dt = ref.select_dt()
+    k = 4
+    (_, _), st, obs = ref.advance(u, ulo, dt, 0, 12, hook_every=4, ktheta=k, max_obs=16)
+    j0, hw = ref.horizon_weights(k)
+    pw = ref.projection_weights()
+    from paper_2010_04760_b200.hwgpu import GpuEvolution
+    gpu = GpuEvolution.from_reference(ref)
+    gpu.set_observers(k, j0, hw, 40, pw)
+    gpu.set_state(u)
+    got = []
+    gpu.advance("ssprk33", dt, 0, 12, every=4, hook=lambda s, tau, ob: got.append((tau[0], ob)))
+    assert len(got) == len(obs) == 4
+    for (tau, ob), row in zip(got, obs):
+        assert abs(tau - row[0]) <= 1e-15
+        vals = [ob["phi"]] + ob["dphi"]
+        for d, v in enumerate(vals):
+            scale = max(abs(row[1 + 2 * d]), abs(row[2 + 2 * d]), 1e-12)
+            assert abs(v.real - row[1 + 2 * d]) <= 1e-6 * scale
+            assert abs(v.imag - row[2 + 2 * d]) <= 1e-6 * scale
+    # multipole projection: compare with the reference's own projection of the slice
+    st = gpu.get_state()
+    ob = gpu.observe()
+    slice_r = np.ascontiguousarray(st[0, 2:-2, 4 + 40])
+    out = np.zeros(1)
+    O.ref_lib().ref_multipole_project(slice_r.ctypes.data_as(O._dp), 8, -2, 0, 2,
+                                      out.ctypes.data_as(O._dp))
+    assert abs(ob["proj"].real - out[0]) <= 1e-12 * max(1.0, abs(out[0]))
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c1_full_1000.npz")),
+                    reason="C1 fixture not generated")
+def test_c1_fp64_1000_steps_vs_reference_full(cuda_ok):
+    """BASELINE gate (1): config C1, GPU fp64 vs reference full (DD) after
+    1000 SSP-RK3 steps within normwise rel. L-inf 1e-12."""
+    import oracle as O
+    fx = load_golden("c1_full_1000")
+    ref = O.RefSolver(O.Physics(a=0.0, spin=0, mmode=0, ell=2, center=3.0, width=0.3), 1024, 64,
+                      mode="full")
+    u, _ = ref.initial_data()
+    dt = (float(fx["dt"][0]), float(fx["dt"][1]))
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
+    gpu = GpuEvolution.from_reference(ref, SchemeSpec("weno5", "f64"))
+    gpu.set_state(u)
+    st = gpu.advance("ssprk33", dt, 0, 1000)
+    assert st["steps_done"] == 1000 and not st["blew_up"]
+    got = interior(gpu.get_state())
+    err = np.max(np.abs(got - fx["state"])) / np.max(np.abs(fx["state"]))
+    assert err <= 1e-12, err
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c2desk_mixed_1000.npz")),
+                    reason="C2 desk fixture not generated")
+def test_c2desk_mixed_1000_steps_vs_reference_mixed(cuda_ok):
+    """BASELINE gate (2): GPU mixed (fp32 weights) vs the reference's own
+    mixed mode (DD + fp64 weights), extremal Kerr s=-2 m=2, 1000 steps: 1e-6."""
+    import oracle as O
+    fx = load_golden("c2desk_mixed_1000")
+    ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22), 1024, 32,
+                      mode="mixed")
+    u, _ = ref.initial_data()
+    dt = (float(fx["dt"][0]), float(fx["dt"][1]))
+    from paper_2010_04760_b200.hwgpu import GpuEvolution
+    gpu = GpuEvolution.from_reference(ref)
+    gpu.set_state(u)
+    st = gpu.advance("ssprk33", dt, 0, 1000)
+    assert st["steps_done"] == 1000 and not st["blew_up"]
+    got = interior(gpu.get_state())
+    err = np.max(np.abs(got - fx["state"])) / np.max(np.abs(fx["state"]))
+    assert err <= 1e-6, err
