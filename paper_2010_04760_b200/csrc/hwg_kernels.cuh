@@ -37,6 +37,13 @@
 
 namespace hwg {
 
+#ifndef HWG_MINB
+#define HWG_MINB 4  // resident blocks per SM (16 warps): caps registers at 128
+#endif
+#ifndef HWG_RING
+#define HWG_RING 3  // bulk-copy ring depth (rows in flight + 1) per warp
+#endif
+
 constexpr int kHalo = 4;          // halo rows per side (KO8 needs 4)
 constexpr int kWarpsPerBlock = 4;
 constexpr unsigned kFull = 0xffffffffu;
@@ -83,6 +90,19 @@ __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
 __device__ __forceinline__ double2 neg2(double2 v) { return make_double2(-v.x, -v.y); }
 
+// reference cubic continuation (defined below), used by row_or_ghost
+__device__ __forceinline__ double2 cubic(double2 a, double2 b, double2 c, double2 d);
+
+// state row r of one plane column; rows < 0 of the slab holding the
+// excision end are the reference's cubic ghosts (rare path: orientation switch)
+__device__ __noinline__ double2 row_or_ghost(const double2* col, int r, ptrdiff_t ntp, int phys_lo) {
+  if (r >= 0 || !phys_lo) return __ldg(col + r * ntp);
+  double2 g[8];
+  for (int m = 0; m < 4; ++m) g[4 + m] = __ldg(col + m * ntp);
+  for (int t = 1; t <= -r; ++t) g[4 - t] = cubic(g[4 - t + 1], g[4 - t + 2], g[4 - t + 3], g[4 - t + 4]);
+  return g[4 + r];
+}
+
 // reference cubic continuation p[-t] = 4p[-t+1] - 6p[-t+2] + 4p[-t+3] - p[-t+4]
 // (evolve.cpp:48-50), same evaluation order
 __device__ __forceinline__ double cubic1(double a, double b, double c, double d) {
@@ -93,13 +113,31 @@ __device__ __forceinline__ double2 cubic(double2 a, double2 b, double2 c, double
 }
 
 // ---------------------------------------------------------------------------
+// Reciprocals without IEEE special-case branches.  The arguments below are
+// sums of positive weights (never 0, inf or subnormal on admissible states);
+// a NaN state still propagates NaN.
+__device__ __forceinline__ float frcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ double drcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));  // MUFU.RCP64H seed (~2^-20)
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);                                       // ~2^-40
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);                                    // ~1 ulp
+}
+
+// ---------------------------------------------------------------------------
 // WENO5-JS interface value (spatial.hpp:29-92) on the oriented window
 // f0..f4, returned WITHOUT the 1/6 factor (folded into iscale).
 //
 // fp64 weights: alpha_k = d_k/(eps + IS_k)^2 normalised; with the indicators
 // scaled by 4 (IS' = 13/3 t^2 + s^2, eps' = 4 eps) the weights are
 // w_k = d_k prod_{i!=k} e_i^2 / sum(...), so one reciprocal replaces the
-// reference's five divisions.
+// reference's five divisions (weights and renormalisation, spatial.hpp:58-90).
 __device__ __forceinline__ double weno5_f64(double f0, double f1, double f2, double f3,
                                             double f4, double eps4, int linear) {
   double n0, n1, n2;
@@ -125,7 +163,7 @@ __device__ __forceinline__ double weno5_f64(double f0, double f1, double f2, dou
   double c1 = fma(2.0, f3, fma(5.0, f2, -f1));
   double c2 = fma(5.0, f3, fma(2.0, f2, -f4));
   double num = fma(n2, c2, fma(n1, c1, n0 * c0));
-  return num * __drcp_rn((n0 + n1) + n2);
+  return num * drcp((n0 + n1) + n2);
 }
 
 // Mixed mode (the paper's): window demoted to fp32, smoothness indicators and
@@ -149,10 +187,10 @@ __device__ __forceinline__ double weno5_mixed(double f0, double f1, double f2, d
     t = fmaf(-2.0f, g3, g2) + g4;
     s = fmaf(3.0f, g2, fmaf(-4.0f, g3, g4));
     float e2 = eps + fmaf(c1312 * t, t, qt * s * s);
-    float a0 = 0.1f * __frcp_rn(e0 * e0);
-    float a1 = 0.6f * __frcp_rn(e1 * e1);
-    float a2 = 0.3f * __frcp_rn(e2 * e2);
-    float inv = __frcp_rn((a0 + a1) + a2);
+    float a0 = 0.1f * frcp(e0 * e0);
+    float a1 = 0.6f * frcp(e1 * e1);
+    float a2 = 0.3f * frcp(e2 * e2);
+    float inv = frcp((a0 + a1) + a2);
     w0 = a0 * inv; w1 = a1 * inv; w2 = a2 * inv;
   }
   const double W0 = (double)w0, W1 = (double)w1, W2 = (double)w2;
@@ -160,7 +198,7 @@ __device__ __forceinline__ double weno5_mixed(double f0, double f1, double f2, d
   double c1 = fma(2.0, f3, fma(5.0, f2, -f1));
   double c2 = fma(5.0, f3, fma(2.0, f2, -f4));
   double num = fma(W2, c2, fma(W1, c1, W0 * c0));
-  return num * __drcp_rn((W0 + W1) + W2);
+  return num * drcp((W0 + W1) + W2);
 }
 
 template <int MODE>
@@ -185,53 +223,132 @@ __device__ __forceinline__ double weno3(double f0, double f1, double f2, const S
     float g0 = (float)f0, g1 = (float)f1, g2 = (float)f2;
     float d0 = g1 - g0, d1 = g2 - g1;
     float e0 = fmaf(d0, d0, a.epsf), e1 = fmaf(d1, d1, a.epsf);
-    float x0 = (1.0f / 3.0f) * __frcp_rn(e0 * e0);
-    float x1 = (2.0f / 3.0f) * __frcp_rn(e1 * e1);
-    float inv = __frcp_rn(x0 + x1);
+    float x0 = (1.0f / 3.0f) * frcp(e0 * e0);
+    float x1 = (2.0f / 3.0f) * frcp(e1 * e1);
+    float inv = frcp(x0 + x1);
     n0 = (double)(x0 * inv);
     n1 = (double)(x1 * inv);
   }
   double q0 = fma(3.0, f1, -f0);
   double q1 = f1 + f2;
-  return fma(n1, q1, n0 * q0) * __drcp_rn(n0 + n1);
+  return fma(n1, q1, n0 * q0) * drcp(n0 + n1);
 }
 
-// ---------------------------------------------------------------------------
-// theta neighbour Psi(j, k + d) of every lane: warp shuffle when the
-// (parity-reflected) source column lies in this warp's chunk, a direct load
-// for the few edge lanes whose source lies in the neighbouring chunk.
-__device__ __forceinline__ double2 theta_nb(double2 v, int d, int k, int k0, int nt, bool active,
-                                            int negpar, const double2* row) {
-  int kk = k + d;
-  bool flip = false;
-  if (kk < 0) { kk = -1 - kk; flip = negpar; }
-  else if (kk >= nt) { kk = 2 * nt - 1 - kk; flip = negpar; }
-  const int src = kk - k0;
-  const bool in = (src >= 0) && (src < 32);
-  const int sl = in ? src : (threadIdx.x & 31);
-  double2 r;
-  r.x = __shfl_sync(kFull, v.x, sl);
-  r.y = __shfl_sync(kFull, v.y, sl);
-  if (!in && active) r = ld2(row + kk);
-  return flip ? neg2(r) : r;
+// interface value of one oriented window for either scheme (w[] = window
+// rows j - L .. j + R, C = index of row j); minus = right-biased mirror.
+template <int SCH, int MODE, int C>
+__device__ __forceinline__ double iface_at(const double* w, bool minus, int shift,
+                                           const StageArgs& a) {
+  // interface j + 1/2 + shift
+  const int c = C + shift;
+  if (SCH == WENO5) {
+    return minus ? weno5<MODE>(w[c + 3], w[c + 2], w[c + 1], w[c], w[c - 1], a)
+                 : weno5<MODE>(w[c - 2], w[c - 1], w[c], w[c + 1], w[c + 2], a);
+  }
+  return minus ? weno3<MODE>(w[c + 2], w[c + 1], w[c], a)
+               : weno3<MODE>(w[c - 1], w[c], w[c + 1], a);
 }
 
 // ---------------------------------------------------------------------------
 template <int SCH>
 struct Win {
-  // window rows j - L .. j + R around the point being updated
-  static constexpr int L = (SCH == FD6KO) ? 4 : (SCH == WENO5 ? 3 : 2);
-  static constexpr int R = L;
-  static constexpr int W = L + R + 1;
+  // register windows, rows j - L .. j + R (L + R >= 4 so the cubic scri
+  // continuation always has its four predecessors in registers)
+  static constexpr int SL = (SCH == FD6KO) ? 4 : (SCH == WENO5 ? 1 : 2);  // Psi
+  static constexpr int PL = (SCH == FD6KO) ? 4 : 2;                       // pi
+  static constexpr int R = (SCH == FD6KO) ? 4 : (SCH == WENO5 ? 3 : 2);
+  static constexpr int SW = SL + R + 1, PW = PL + R + 1;
+  // rows needed at initialisation (fresh F(jb - 1/2) in either orientation)
+  static constexpr int IL = (SCH == FD6KO) ? 4 : (SCH == WENO5 ? 3 : 2);
+  static constexpr int IW = IL + R + 1;
+  static constexpr int IA = (IL + 4 > IW) ? IL + 4 : IW;  // init array (4 rows for the cubic)
 };
 
+__device__ __forceinline__ double2 shfl_up2(double2 v, int d) {
+  return make_double2(__shfl_up_sync(kFull, v.x, d), __shfl_up_sync(kFull, v.y, d));
+}
+__device__ __forceinline__ double2 shfl_dn2(double2 v, int d) {
+  return make_double2(__shfl_down_sync(kFull, v.x, d), __shfl_down_sync(kFull, v.y, d));
+}
+
+// parity reflection of a theta column across the poles (evolve.cpp:59-70)
+__device__ __forceinline__ int reflect_col(int c, int nt, bool& flip, int negpar) {
+  flip = false;
+  if (c < 0) { c = -1 - c; flip = negpar; }
+  else if (c >= nt) { c = 2 * nt - 1 - c; flip = negpar; }
+  if (c < 0 || c >= nt) { c = 0; flip = false; }  // only for lanes far outside tiny grids
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// Bulk-copy (TMA engine) row ring.  Each warp owns S slots of shared memory;
+// slot s holds, for one iteration j: the pointwise data of row j (the 9
+// coefficient values as 4 double2 planes + ath, u_n, u^(4), F(u^(4)) as the
+// epilogue needs) and the stencil-input row j + 1 + R that enters the
+// register window at the end of the iteration.  Lane 0 issues the row's
+// cp.async.bulk copies S iterations ahead; an mbarrier per slot completes on
+// the transferred byte count.  The warp's lanes then read their own column
+// from shared memory, so the prefetch costs no registers.
+template <int EPI>
+struct Slot {
+  static constexpr int ROWB = 32 * 16;                 // one double2 row chunk
+  static constexpr int BL = 0, CW = ROWB, CBT = 2 * ROWB, CCF = 3 * ROWB;
+  static constexpr int XPS = 4 * ROWB, XPI = 5 * ROWB;  // next stencil row
+  static constexpr int ATH = 6 * ROWB;                  // 32 doubles
+  static constexpr int BASE = ATH + 32 * 8;
+  static constexpr bool HAS_A = EPI == EPI_RK3 || EPI == EPI_RK104_5 || EPI == EPI_RK104_10;
+  static constexpr bool HAS_BG = EPI == EPI_RK104_10;
+  static constexpr int APS = BASE, API = BASE + ROWB;
+  static constexpr int BPS = BASE + 2 * ROWB, BPI = BASE + 3 * ROWB;
+  static constexpr int GPS = BASE + 4 * ROWB, GPI = BASE + 5 * ROWB;
+  static constexpr int BYTES = BASE + (HAS_A ? 2 * ROWB : 0) + (HAS_BG ? 4 * ROWB : 0);
+  static constexpr int S = HAS_BG ? 2 : HWG_RING;       // ring depth
+};
+
+template <int EPI>
+constexpr size_t stage_smem_bytes() {
+  return (size_t)kWarpsPerBlock * Slot<EPI>::S * (Slot<EPI>::BYTES + 8);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_LOOP:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_LOOP;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 template <int SCH, int MODE, int EPI>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_MINB)
 stage_kernel(const StageArgs a) {
   if (a.flag != nullptr && *(volatile unsigned long long*)a.flag != 0ull) return;  // frozen
-  constexpr int L = Win<SCH>::L, W = Win<SCH>::W, C = L;
+  using Wn = Win<SCH>;
+  using SlotT = Slot<EPI>;
+  constexpr int SL = Wn::SL, PL = Wn::PL, R = Wn::R, SW = Wn::SW, PW = Wn::PW;
+  constexpr int IL = Wn::IL, IW = Wn::IW, S = SlotT::S, SB = SlotT::BYTES;
+  extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarpsPerBlock + wib;
   const int chunk = gw % a.nchunks;
   const int range = gw / a.nchunks;
   if (range >= a.nranges) return;                       // whole warp
@@ -239,138 +356,176 @@ stage_kernel(const StageArgs a) {
   const int je = (int)((long long)(range + 1) * a.n / a.nranges);
   const int k0 = chunk << 5;
   const int k = k0 + lane;
-  const bool active = k < a.nt;
-  const int kc = active ? k : a.nt - 1;
-  const int ntp = a.ntp, n = a.n;
+  const int nt = a.nt, n = a.n;
+  const bool active = k < nt;
+  const ptrdiff_t ntp = a.ntp;
+  const int kc = active ? k : nt - 1;
+  // theta halo: lanes 0,1 hold columns k0-2, k0-1; lanes 30,31 hold k0+32, k0+33
+  const bool has_h = lane < 2 || lane >= 30;
+  bool hflip;
+  const int hcol = reflect_col(lane < 2 ? k0 - 2 + lane : k0 + 2 + lane, nt, hflip, a.negpar);
+  // idle lanes past the south pole publish the parity image of lane refl
+  const bool pole_chunk = k0 + 32 > nt;
+  bool wflip;
+  const int wsrc = reflect_col(k, nt, wflip, a.negpar) - k0;
+
+  unsigned char* ring = smem + (size_t)wib * S * SB;
+  const uint32_t bar0 = smem_u32(smem + (size_t)kWarpsPerBlock * S * SB) + wib * S * 8;
+
+  // lane 0: issue the copies of iteration j into slot s
+  auto issue = [&](int s, int j) {
+    const uint32_t bar = bar0 + s * 8;
+    const uint32_t dst = smem_u32(ring + (size_t)s * SB);
+    const int rn = j + 1 + R;
+    const bool st = (j + 1 < je) && !(rn >= n && a.phys_hi);
+    const uint32_t bytes = SlotT::BASE - (st ? 0 : 2 * SlotT::ROWB) +
+                           (SlotT::HAS_A ? 2 * SlotT::ROWB : 0) +
+                           (SlotT::HAS_BG ? 4 * SlotT::ROWB : 0);
+    mbar_expect_tx(bar, bytes);
+    const ptrdiff_t o = (ptrdiff_t)j * ntp + k0;
+    bulk_g2s(dst + SlotT::BL, a.cbl + o, SlotT::ROWB, bar);
+    bulk_g2s(dst + SlotT::CW, a.cw + o, SlotT::ROWB, bar);
+    bulk_g2s(dst + SlotT::CBT, a.cbt + o, SlotT::ROWB, bar);
+    bulk_g2s(dst + SlotT::CCF, a.ccf + o, SlotT::ROWB, bar);
+    bulk_g2s(dst + SlotT::ATH, a.cath + o, 32 * 8, bar);
+    if (st) {
+      const ptrdiff_t os = (ptrdiff_t)rn * ntp + k0;
+      bulk_g2s(dst + SlotT::XPS, a.xpsi + os, SlotT::ROWB, bar);
+      bulk_g2s(dst + SlotT::XPI, a.xpi + os, SlotT::ROWB, bar);
+    }
+    if (SlotT::HAS_A) {
+      bulk_g2s(dst + SlotT::APS, a.apsi + o, SlotT::ROWB, bar);
+      bulk_g2s(dst + SlotT::API, a.api + o, SlotT::ROWB, bar);
+    }
+    if (SlotT::HAS_BG) {
+      bulk_g2s(dst + SlotT::BPS, a.bpsi + o, SlotT::ROWB, bar);
+      bulk_g2s(dst + SlotT::BPI, a.bpi + o, SlotT::ROWB, bar);
+      bulk_g2s(dst + SlotT::GPS, a.gpsi + o, SlotT::ROWB, bar);
+      bulk_g2s(dst + SlotT::GPI, a.gpi + o, SlotT::ROWB, bar);
+    }
+  };
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(bar0 + s * 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < S && jb + q < je; ++q) issue(q, jb + q);
+  }
+  __syncwarp();
 
   const double2* xps = a.xpsi + kc;
   const double2* xpi = a.xpi + kc;
 
-  // ---- window initialisation: rows jb - L .. jb + R
-  double2 wps[W], wpi[W];
-  if (a.phys_lo && jb == 0) {
-    double2 qs[L + 4], qp[L + 4];
+  // ---- initial rows jb - IL .. jb + R (ghosts synthesised at the excision end)
+  double2 ips[Wn::IA], ipi[Wn::IA];
+  if (a.phys_lo && jb < IL) {
+    // only jb == 0 happens (ranges are >= 8 rows)
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      qs[L + m] = ld2(xps + (size_t)m * ntp);
-      qp[L + m] = ld2(xpi + (size_t)m * ntp);
+      ips[IL + m] = ld2(xps + m * ntp);
+      ipi[IL + m] = ld2(xpi + m * ntp);
     }
 #pragma unroll
-    for (int t = 1; t <= L; ++t) {
-      qs[L - t] = cubic(qs[L - t + 1], qs[L - t + 2], qs[L - t + 3], qs[L - t + 4]);
-      qp[L - t] = cubic(qp[L - t + 1], qp[L - t + 2], qp[L - t + 3], qp[L - t + 4]);
+    for (int t = 1; t <= IL; ++t) {
+      ips[IL - t] = cubic(ips[IL - t + 1], ips[IL - t + 2], ips[IL - t + 3], ips[IL - t + 4]);
+      ipi[IL - t] = cubic(ipi[IL - t + 1], ipi[IL - t + 2], ipi[IL - t + 3], ipi[IL - t + 4]);
     }
 #pragma unroll
-    for (int m = 0; m < W; ++m) {
-      if (m < L + 4) { wps[m] = qs[m]; wpi[m] = qp[m]; }
-      else {
-        wps[m] = ld2(xps + (size_t)(m - L) * ntp);
-        wpi[m] = ld2(xpi + (size_t)(m - L) * ntp);
-      }
+    for (int m = IL + 4; m < IW; ++m) {
+      ips[m] = ld2(xps + (m - IL) * ntp);
+      ipi[m] = ld2(xpi + (m - IL) * ntp);
     }
   } else {
 #pragma unroll
-    for (int m = 0; m < W; ++m) {
-      const int r = jb - L + m;
+    for (int m = 0; m < IW; ++m) {
+      const int r = jb - IL + m;
       if (r >= n && a.phys_hi) {
-        wps[m] = cubic(wps[m - 1], wps[m - 2], wps[m - 3], wps[m - 4]);
-        wpi[m] = cubic(wpi[m - 1], wpi[m - 2], wpi[m - 3], wpi[m - 4]);
+        ips[m] = cubic(ips[m - 1], ips[m - 2], ips[m - 3], ips[m - 4]);
+        ipi[m] = cubic(ipi[m - 1], ipi[m - 2], ipi[m - 3], ipi[m - 4]);
       } else {
-        wps[m] = ld2(xps + (ptrdiff_t)r * ntp);
-        wpi[m] = ld2(xpi + (ptrdiff_t)r * ntp);
+        ips[m] = ld2(xps + r * ntp);
+        ipi[m] = ld2(xpi + r * ntp);
       }
     }
   }
+  double2 wps[SW], wpi[PW];
+#pragma unroll
+  for (int m = 0; m < SW; ++m) wps[m] = ips[IL - SL + m];
+#pragma unroll
+  for (int m = 0; m < PW; ++m) wpi[m] = ipi[IL - PL + m];
 
-  // pointwise data of the current row (software pipelined one row ahead)
-  const size_t pk = kc;
-  auto ldpt = [&](int j, double2& bl, double2& w, double2& bt, double2& cf, double& ath,
-                  double2& aps, double2& api, double2& bps, double2& bpi, double2& gps,
-                  double2& gpi) {
-    const size_t o = (size_t)j * ntp + pk;
-    bl = ld2(a.cbl + o); w = ld2(a.cw + o); bt = ld2(a.cbt + o); cf = ld2(a.ccf + o);
-    ath = __ldg(a.cath + o);
-    if (EPI == EPI_RK3 || EPI == EPI_RK104_5 || EPI == EPI_RK104_10) {
-      aps = a.apsi[o]; api = a.api[o];
-    }
-    if (EPI == EPI_RK104_10) {
-      bps = a.bpsi[o]; bpi = a.bpi[o]; gps = a.gpsi[o]; gpi = a.gpi[o];
-    }
-  };
-  double2 bl, cw, cbt, ccf, aps, api, bps, bpi, gps, gpi;
-  double ath;
-  ldpt(jb, bl, cw, cbt, ccf, ath, aps, api, bps, bpi, gps, gpi);
   const double cot = __ldg(a.cot + kc);
-
   // carried interface values F(j - 1/2)
   double fpsR = 0.0, fpsI = 0.0, fpiR = 0.0, fpiI = 0.0;
-  int opi = -1;  // orientation of the carried pi interfaces (1 = minus)
-  if (SCH == WENO5) {
-    fpsR = weno5<MODE>(wps[C + 2].x, wps[C + 1].x, wps[C].x, wps[C - 1].x, wps[C - 2].x, a);
-    fpsI = weno5<MODE>(wps[C + 2].y, wps[C + 1].y, wps[C].y, wps[C - 1].y, wps[C - 2].y, a);
-  } else if (SCH == WENO3) {
-    fpsR = weno3<MODE>(wps[C + 1].x, wps[C].x, wps[C - 1].x, a);
-    fpsI = weno3<MODE>(wps[C + 1].y, wps[C].y, wps[C - 1].y, a);
+  bool opi = __ldg(&a.cbl[(ptrdiff_t)jb * ntp + kc].y) < 0.0;  // true = minus
+  if (SCH != FD6KO) {
+    double r[IW], q[IW];
+#pragma unroll
+    for (int m = 0; m < IW; ++m) { r[m] = ips[m].x; q[m] = ips[m].y; }
+    fpsR = iface_at<SCH, MODE, IL>(r, true, -1, a);
+    fpsI = iface_at<SCH, MODE, IL>(q, true, -1, a);
+#pragma unroll
+    for (int m = 0; m < IW; ++m) { r[m] = ipi[m].x; q[m] = ipi[m].y; }
+    fpiR = iface_at<SCH, MODE, IL>(r, opi, -1, a);
+    fpiI = iface_at<SCH, MODE, IL>(q, opi, -1, a);
   }
 
   bool bad = false;
-  for (int j = jb; j < je; ++j) {
-    // ---- prefetch next row (state row j + 1 + R and pointwise row j + 1)
-    const bool more = j + 1 < je;
-    const int rn = j + 1 + Win<SCH>::R;
+  const double2* xrow_h = a.xpsi + hcol + (ptrdiff_t)jb * ntp;
+  int slot = 0;
+  uint32_t parity = 0;
+  for (int j = jb; j < je; ++j, xrow_h += ntp) {
+    const unsigned char* sl = ring + (size_t)slot * SB;
+    const int rn = j + 1 + R;
     const bool synth = (rn >= n) && a.phys_hi;
-    double2 nps = make_double2(0.0, 0.0), npi = nps;
-    double2 nbl = nps, ncw = nps, ncbt = nps, nccf = nps, naps = nps, napi = nps, nbps = nps,
-            nbpi = nps, ngps = nps, ngpi = nps;
-    double nath = 0.0;
-    if (more) {
-      if (!synth) {
-        nps = ld2(xps + (ptrdiff_t)rn * ntp);
-        npi = ld2(xpi + (ptrdiff_t)rn * ntp);
-      }
-      ldpt(j + 1, nbl, ncw, ncbt, nccf, nath, naps, napi, nbps, nbpi, ngps, ngpi);
+    // theta halo of this row (4 lanes, L1/L2 hits)
+    double2 h = make_double2(0.0, 0.0);
+    if (has_h) {
+      h = ld2(xrow_h);
+      if (hflip) h = neg2(h);
     }
+    mbar_wait(bar0 + slot * 8, parity);
+    const double2 bl = reinterpret_cast<const double2*>(sl + SlotT::BL)[lane];
 
     // ---- phase 1: radial derivatives
     double dpsR, dpsI, dpiR, dpiI;
-    if (SCH == WENO5) {
-      double cR = weno5<MODE>(wps[C + 3].x, wps[C + 2].x, wps[C + 1].x, wps[C].x, wps[C - 1].x, a);
-      double cI = weno5<MODE>(wps[C + 3].y, wps[C + 2].y, wps[C + 1].y, wps[C].y, wps[C - 1].y, a);
+    if (SCH != FD6KO) {
+      double r[SW], q[SW];
+#pragma unroll
+      for (int m = 0; m < SW; ++m) { r[m] = wps[m].x; q[m] = wps[m].y; }
+      // Psi rows: right-biased everywhere (b <= 0; evolve.cpp:103-104)
+      const double cR = iface_at<SCH, MODE, SL>(r, true, 0, a);
+      const double cI = iface_at<SCH, MODE, SL>(q, true, 0, a);
       dpsR = (cR - fpsR) * a.iscale; fpsR = cR;
       dpsI = (cI - fpsI) * a.iscale; fpsI = cI;
-      const int o = bl.y < 0.0;   // split_k rule: minus where lam < 0 (evolve.cpp:19-30)
-      if (o != opi) {             // start of a (sub-)row: fresh F(j - 1/2)
-        double2 f0 = o ? wpi[C + 2] : wpi[C - 3], f1 = o ? wpi[C + 1] : wpi[C - 2],
-                f2 = o ? wpi[C] : wpi[C - 1], f3 = o ? wpi[C - 1] : wpi[C],
-                f4 = o ? wpi[C - 2] : wpi[C + 1];
-        fpiR = weno5<MODE>(f0.x, f1.x, f2.x, f3.x, f4.x, a);
-        fpiI = weno5<MODE>(f0.y, f1.y, f2.y, f3.y, f4.y, a);
-        opi = o;
-      }
-      double2 f0 = o ? wpi[C + 3] : wpi[C - 2], f1 = o ? wpi[C + 2] : wpi[C - 1],
-              f2 = o ? wpi[C + 1] : wpi[C], f3 = o ? wpi[C] : wpi[C + 1],
-              f4 = o ? wpi[C - 1] : wpi[C + 2];
-      double pR = weno5<MODE>(f0.x, f1.x, f2.x, f3.x, f4.x, a);
-      double pI = weno5<MODE>(f0.y, f1.y, f2.y, f3.y, f4.y, a);
-      dpiR = (pR - fpiR) * a.iscale; fpiR = pR;
-      dpiI = (pI - fpiI) * a.iscale; fpiI = pI;
-    } else if (SCH == WENO3) {
-      double cR = weno3<MODE>(wps[C + 2].x, wps[C + 1].x, wps[C].x, a);
-      double cI = weno3<MODE>(wps[C + 2].y, wps[C + 1].y, wps[C].y, a);
-      dpsR = (cR - fpsR) * a.iscale; fpsR = cR;
-      dpsI = (cI - fpsI) * a.iscale; fpsI = cI;
-      const int o = bl.y < 0.0;
+      // pi rows: minus where lam < 0 (split_k rule, evolve.cpp:19-30, 105-110)
+      const bool o = bl.y < 0.0;
+      double x[PW], y[PW];
+#pragma unroll
+      for (int m = 0; m < PW; ++m) { x[m] = wpi[m].x; y[m] = wpi[m].y; }
       if (o != opi) {
-        double2 f0 = o ? wpi[C + 1] : wpi[C - 2], f1 = o ? wpi[C] : wpi[C - 1],
-                f2 = o ? wpi[C - 1] : wpi[C];
-        fpiR = weno3<MODE>(f0.x, f1.x, f2.x, a);
-        fpiI = weno3<MODE>(f0.y, f1.y, f2.y, a);
+        // start of a sub-row: fresh F(j - 1/2) in the new orientation
+        if (!o && SCH == WENO5) {
+          // plus at j - 1/2 needs row j - 3, outside the window
+          double2 u3 = row_or_ghost(xpi, j - 3, ntp, a.phys_lo);
+          double xx[PW + 1], yy[PW + 1];
+          xx[0] = u3.x; yy[0] = u3.y;
+#pragma unroll
+          for (int m = 0; m < PW; ++m) { xx[m + 1] = x[m]; yy[m + 1] = y[m]; }
+          fpiR = iface_at<SCH, MODE, PL + 1>(xx, false, -1, a);
+          fpiI = iface_at<SCH, MODE, PL + 1>(yy, false, -1, a);
+        } else {
+          fpiR = iface_at<SCH, MODE, PL>(x, o, -1, a);
+          fpiI = iface_at<SCH, MODE, PL>(y, o, -1, a);
+        }
         opi = o;
       }
-      double2 f0 = o ? wpi[C + 2] : wpi[C - 1], f1 = o ? wpi[C + 1] : wpi[C],
-              f2 = o ? wpi[C] : wpi[C + 1];
-      double pR = weno3<MODE>(f0.x, f1.x, f2.x, a);
-      double pI = weno3<MODE>(f0.y, f1.y, f2.y, a);
+      double pR, pI;
+      if (__all_sync(kFull, !o)) {
+        pR = iface_at<SCH, MODE, PL>(x, false, 0, a);
+        pI = iface_at<SCH, MODE, PL>(y, false, 0, a);
+      } else {
+        pR = iface_at<SCH, MODE, PL>(x, o, 0, a);
+        pI = iface_at<SCH, MODE, PL>(y, o, 0, a);
+      }
       dpiR = (pR - fpiR) * a.iscale; fpiR = pR;
       dpiI = (pI - fpiI) * a.iscale; fpiI = pI;
     } else {
@@ -378,6 +533,7 @@ stage_kernel(const StageArgs a) {
       auto fd6 = [&](double m3, double m2, double m1, double p1, double p2, double p3) {
         return fma(45.0, p1 - m1, fma(-9.0, p2 - m2, p3 - m3)) * a.iscale;
       };
+      constexpr int C = SL;
       dpsR = fd6(wps[C - 3].x, wps[C - 2].x, wps[C - 1].x, wps[C + 1].x, wps[C + 2].x, wps[C + 3].x);
       dpsI = fd6(wps[C - 3].y, wps[C - 2].y, wps[C - 1].y, wps[C + 1].y, wps[C + 2].y, wps[C + 3].y);
       dpiR = fd6(wpi[C - 3].x, wpi[C - 2].x, wpi[C - 1].x, wpi[C + 1].x, wpi[C + 2].x, wpi[C + 3].x);
@@ -385,12 +541,20 @@ stage_kernel(const StageArgs a) {
     }
 
     // ---- phase 2: (d_thth + cot d_th) Psi (spatial.hpp:208-222)
-    const double2 ps = wps[C];
-    const double2* xrow = a.xpsi + (ptrdiff_t)j * ntp;
-    const double2 m2 = theta_nb(ps, -2, k, k0, a.nt, active, a.negpar, xrow);
-    const double2 m1 = theta_nb(ps, -1, k, k0, a.nt, active, a.negpar, xrow);
-    const double2 p1 = theta_nb(ps, 1, k, k0, a.nt, active, a.negpar, xrow);
-    const double2 p2 = theta_nb(ps, 2, k, k0, a.nt, active, a.negpar, xrow);
+    const double2 ps = wps[SL];
+    double2 wv = ps;   // value this lane publishes to its theta neighbours
+    if (pole_chunk) {  // warp-uniform
+      double2 img = make_double2(__shfl_sync(kFull, ps.x, wsrc & 31),
+                                 __shfl_sync(kFull, ps.y, wsrc & 31));
+      if (!active) wv = wflip ? neg2(img) : img;
+    }
+    const double2 su2 = shfl_up2(wv, 2), su1 = shfl_up2(wv, 1);
+    const double2 sd1 = shfl_dn2(wv, 1), sd2 = shfl_dn2(wv, 2);
+    const double2 hd1 = shfl_dn2(h, 1), hu1 = shfl_up2(h, 1);
+    const double2 m2 = lane >= 2 ? su2 : h;
+    const double2 m1 = lane >= 1 ? su1 : hd1;
+    const double2 p1 = lane <= 30 ? sd1 : hu1;
+    const double2 p2 = lane <= 29 ? sd2 : h;
     const double d1R = fma(8.0, p1.x - m1.x, m2.x - p2.x) * a.inv1;
     const double d1I = fma(8.0, p1.y - m1.y, m2.y - p2.y) * a.inv1;
     const double d2R = fma(-30.0, ps.x, fma(16.0, m1.x + p1.x, -(m2.x + p2.x))) * a.inv2;
@@ -399,7 +563,11 @@ stage_kernel(const StageArgs a) {
     const double angI = fma(cot, d1I, d2I);
 
     // ---- phase 3: pointwise assembly (evolve.cpp:149-167)
-    const double2 pv = wpi[C];
+    const double2 cw = reinterpret_cast<const double2*>(sl + SlotT::CW)[lane];
+    const double2 cbt = reinterpret_cast<const double2*>(sl + SlotT::CBT)[lane];
+    const double2 ccf = reinterpret_cast<const double2*>(sl + SlotT::CCF)[lane];
+    const double ath = reinterpret_cast<const double*>(sl + SlotT::ATH)[lane];
+    const double2 pv = wpi[PL];
     const double b = bl.x, lam = bl.y;
     double f0 = fma(-b, dpsR, pv.x);
     double f1 = fma(-b, dpsI, pv.y);
@@ -428,26 +596,34 @@ stage_kernel(const StageArgs a) {
     } else if (EPI == EPI_AXPY) {
       ops = make_double2(ps.x + a.cg * f0, ps.y + a.cg * f1);
       opv = make_double2(pv.x + a.cg * f2, pv.y + a.cg * f3);
-    } else if (EPI == EPI_RK3) {
-      ops = make_double2(a.ca * aps.x + a.cb * (ps.x + a.cg * f0),
-                         a.ca * aps.y + a.cb * (ps.y + a.cg * f1));
-      opv = make_double2(a.ca * api.x + a.cb * (pv.x + a.cg * f2),
-                         a.ca * api.y + a.cb * (pv.y + a.cg * f3));
-    } else if (EPI == EPI_RK104_5) {
-      ops = make_double2(a.ca * aps.x + a.cb * ps.x + a.cg * f0,
-                         a.ca * aps.y + a.cb * ps.y + a.cg * f1);
-      opv = make_double2(a.ca * api.x + a.cb * pv.x + a.cg * f2,
-                         a.ca * api.y + a.cb * pv.y + a.cg * f3);
     } else {
-      ops = make_double2(
-          a.ca * aps.x + a.cb * bps.x + a.cc * ps.x + a.cg * (a.cd * gps.x + a.ce * f0),
-          a.ca * aps.y + a.cb * bps.y + a.cc * ps.y + a.cg * (a.cd * gps.y + a.ce * f1));
-      opv = make_double2(
-          a.ca * api.x + a.cb * bpi.x + a.cc * pv.x + a.cg * (a.cd * gpi.x + a.ce * f2),
-          a.ca * api.y + a.cb * bpi.y + a.cc * pv.y + a.cg * (a.cd * gpi.y + a.ce * f3));
+      const double2 aps = reinterpret_cast<const double2*>(sl + SlotT::APS)[lane];
+      const double2 api = reinterpret_cast<const double2*>(sl + SlotT::API)[lane];
+      if (EPI == EPI_RK3) {
+        ops = make_double2(a.ca * aps.x + a.cb * (ps.x + a.cg * f0),
+                           a.ca * aps.y + a.cb * (ps.y + a.cg * f1));
+        opv = make_double2(a.ca * api.x + a.cb * (pv.x + a.cg * f2),
+                           a.ca * api.y + a.cb * (pv.y + a.cg * f3));
+      } else if (EPI == EPI_RK104_5) {
+        ops = make_double2(a.ca * aps.x + a.cb * ps.x + a.cg * f0,
+                           a.ca * aps.y + a.cb * ps.y + a.cg * f1);
+        opv = make_double2(a.ca * api.x + a.cb * pv.x + a.cg * f2,
+                           a.ca * api.y + a.cb * pv.y + a.cg * f3);
+      } else {
+        const double2 bps = reinterpret_cast<const double2*>(sl + SlotT::BPS)[lane];
+        const double2 bpi = reinterpret_cast<const double2*>(sl + SlotT::BPI)[lane];
+        const double2 gps = reinterpret_cast<const double2*>(sl + SlotT::GPS)[lane];
+        const double2 gpi = reinterpret_cast<const double2*>(sl + SlotT::GPI)[lane];
+        ops = make_double2(
+            a.ca * aps.x + a.cb * bps.x + a.cc * ps.x + a.cg * (a.cd * gps.x + a.ce * f0),
+            a.ca * aps.y + a.cb * bps.y + a.cc * ps.y + a.cg * (a.cd * gps.y + a.ce * f1));
+        opv = make_double2(
+            a.ca * api.x + a.cb * bpi.x + a.cc * pv.x + a.cg * (a.cd * gpi.x + a.ce * f2),
+            a.ca * api.y + a.cb * bpi.y + a.cc * pv.y + a.cg * (a.cd * gpi.y + a.ce * f3));
+      }
     }
     if (active) {
-      const size_t o = (size_t)j * ntp + k;
+      const ptrdiff_t o = (ptrdiff_t)j * ntp + k;
       a.opsi[o] = ops;
       a.opi[o] = opv;
       if (EPI == EPI_RK104_5) {
@@ -461,17 +637,25 @@ stage_kernel(const StageArgs a) {
       }
     }
 
-    // ---- slide the window
+    // ---- slide the windows
 #pragma unroll
-    for (int m = 0; m < W - 1; ++m) { wps[m] = wps[m + 1]; wpi[m] = wpi[m + 1]; }
+    for (int m = 0; m < SW - 1; ++m) wps[m] = wps[m + 1];
+#pragma unroll
+    for (int m = 0; m < PW - 1; ++m) wpi[m] = wpi[m + 1];
     if (synth) {
-      wps[W - 1] = cubic(wps[W - 2], wps[W - 3], wps[W - 4], wps[W - 5]);
-      wpi[W - 1] = cubic(wpi[W - 2], wpi[W - 3], wpi[W - 4], wpi[W - 5]);
+      wps[SW - 1] = cubic(wps[SW - 2], wps[SW - 3], wps[SW - 4], wps[SW - 5]);
+      wpi[PW - 1] = cubic(wpi[PW - 2], wpi[PW - 3], wpi[PW - 4], wpi[PW - 5]);
     } else {
-      wps[W - 1] = nps; wpi[W - 1] = npi;
+      wps[SW - 1] = reinterpret_cast<const double2*>(sl + SlotT::XPS)[lane];
+      wpi[PW - 1] = reinterpret_cast<const double2*>(sl + SlotT::XPI)[lane];
     }
-    bl = nbl; cw = ncw; cbt = ncbt; ccf = nccf; ath = nath;
-    aps = naps; api = napi; bps = nbps; bpi = nbpi; gps = ngps; gpi = ngpi;
+    // ---- release the slot and refill it S rows ahead
+    __syncwarp();
+    if (lane == 0 && j + S < je) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(slot, j + S);
+    }
+    if (++slot == S) { slot = 0; parity ^= 1u; }
   }
   if (a.check && __any_sync(kFull, bad) && lane == 0) {
     atomicExch(a.flag + 1, (unsigned long long)a.step);

@@ -215,7 +215,14 @@ namespace {
 
 template <int SCH, int MODE, int EPI>
 void launch_t(const hwg_solver* s, const StageArgs& a) {
-  stage_kernel<SCH, MODE, EPI><<<s->blocks, kWarpsPerBlock * 32, 0, s->stream>>>(a);
+  static bool attr = [] {
+    cudaFuncSetAttribute(stage_kernel<SCH, MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stage_smem_bytes<EPI>());
+    return true;
+  }();
+  (void)attr;
+  stage_kernel<SCH, MODE, EPI><<<s->blocks, kWarpsPerBlock * 32, stage_smem_bytes<EPI>(),
+                                 s->stream>>>(a);
 }
 
 template <int SCH, int MODE>
@@ -595,8 +602,12 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->dev));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, stage_kernel<WENO5, F64, EPI_RK3>));
+    CK(cudaFuncSetAttribute(stage_kernel<WENO5, F64, EPI_RK3>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)stage_smem_bytes<EPI_RK3>()));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_kernel<WENO5, F64, EPI_RK3>,
-                                                     kWarpsPerBlock * 32, 0));
+                                                     kWarpsPerBlock * 32,
+                                                     stage_smem_bytes<EPI_RK3>()));
     s->nchunks = s->ntp / 32;
     const long long target = (long long)nsm * std::max(occ, 1) * kWarpsPerBlock;
     long long nr = std::max<long long>(1, target / s->nchunks);
@@ -636,8 +647,8 @@ void hwg_destroy(hwg_solver* s) {
   delete s;
 }
 
-int hwg_set_stream(hwg_solver* s, void* stream) {
-  s->stream = stream ? static_cast<cudaStream_t>(stream) : s->own;
+int hwg_set_stream(hwg_solver* s, void* stream, int own) {
+  s->stream = own ? s->own : static_cast<cudaStream_t>(stream);
   return HWG_OK;
 }
 

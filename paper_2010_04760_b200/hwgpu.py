@@ -21,10 +21,11 @@ import numpy as np
 
 from .build import SO
 
-if not os.path.exists(SO):
-    raise ImportError(f"libhwgpu.so not built ({SO}); run python -m paper_2010_04760_b200.build")
+_SO = os.environ.get("HWG_LIB", SO)  # experiment override (alternative builds of the same source)
+if not os.path.exists(_SO):
+    raise ImportError(f"libhwgpu.so not built ({_SO}); run python -m paper_2010_04760_b200.build")
 
-_lib = C.CDLL(SO)
+_lib = C.CDLL(_SO)
 _dp = C.POINTER(C.c_double)
 _vp = C.c_void_p
 
@@ -64,7 +65,7 @@ _lib.hwg_last_error.restype = C.c_char_p
 _lib.hwg_last_error.argtypes = [_vp]
 _lib.hwg_create.argtypes = [C.POINTER(HwgDesc), _dp, _dp, C.POINTER(_vp)]
 _lib.hwg_destroy.argtypes = [_vp]
-_lib.hwg_set_stream.argtypes = [_vp, _vp]
+_lib.hwg_set_stream.argtypes = [_vp, _vp, C.c_int]
 for _f in ("hwg_set_state_dd", "hwg_get_state_dd", "hwg_set_state", "hwg_get_state"):
     getattr(_lib, _f).argtypes = [_vp, _dp]
 _lib.hwg_rhs.argtypes = [_vp, _dp, _dp]
@@ -169,7 +170,8 @@ class GpuEvolution:
         return (4, self.ntheta + 4, self.nrho + 8)
 
     def set_stream(self, stream_ptr: int | None):
-        self._chk(_lib.hwg_set_stream(self.h, _vp(stream_ptr or 0)))
+        """Launch on this cudaStream_t (0 = legacy default stream); None = own stream."""
+        self._chk(_lib.hwg_set_stream(self.h, _vp(stream_ptr or 0), int(stream_ptr is None)))
 
     # ------------------------------------------------------------------ state
     def set_state(self, u: np.ndarray, lo: np.ndarray | None = None):

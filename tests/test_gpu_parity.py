@@ -120,16 +120,19 @@ def test_blowup_freezes_state(cuda_ok):
     assert st["blew_up"] and st["blowup_step"] == 1 and st["steps_done"] == 1
     assert seen == [0]
     frozen = gpu.get_state()
-    orc = oracle_from_golden(g, "mixed")
-    uo, _ = orc.advance(u, dt[0], 0, 5)
-    assert rel_linf(frozen, uo) <= 1e-6
+    # the frozen state is exactly the state after the first (inadmissible) step
+    one = gpu_from_golden(g, "mixed")
+    one.set_state(u)
+    one.launch_steps("ssprk33", dt, 0, 1)
+    np.testing.assert_array_equal(interior(frozen), interior(one.get_state()))
+    assert not np.all(np.isfinite(interior(frozen))) or np.max(np.abs(interior(frozen))) > 1e30
 
 
 def test_observers_match_reference(cuda_ok):
     import oracle as O
     if not O.ref_available():
         pytest.skip("reference library not built")
-    ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=0), 128, 8, mode="mixed")
+    ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=0), 128, 8, mode="full")
     u, ulo = ref.initial_data(O.Physics(a=1.0, spin=-2, mmode=0, center=3.0, width=0.5))
     dt = ref.select_dt()
     k = 4
@@ -137,7 +140,7 @@ def test_observers_match_reference(cuda_ok):
     j0, hw = ref.horizon_weights(k)
     pw = ref.projection_weights()
     from paper_2010_04760_b200.hwgpu import GpuEvolution
-    gpu = GpuEvolution.from_reference(ref)
+    gpu = GpuEvolution.from_reference(ref)  # full -> GPU f64 tier
     gpu.set_observers(k, j0, hw, 40, pw)
     gpu.set_state(u)
     got = []
@@ -148,8 +151,8 @@ def test_observers_match_reference(cuda_ok):
         vals = [ob["phi"]] + ob["dphi"]
         for d, v in enumerate(vals):
             scale = max(abs(row[1 + 2 * d]), abs(row[2 + 2 * d]), 1e-12)
-            assert abs(v.real - row[1 + 2 * d]) <= 1e-6 * scale
-            assert abs(v.imag - row[2 + 2 * d]) <= 1e-6 * scale
+            assert abs(v.real - row[1 + 2 * d]) <= 1e-11 * scale
+            assert abs(v.imag - row[2 + 2 * d]) <= 1e-11 * scale
     # multipole projection: compare with the reference's own projection of the slice
     st = gpu.get_state()
     ob = gpu.observe()
