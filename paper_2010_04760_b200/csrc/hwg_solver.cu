@@ -76,12 +76,12 @@ struct hwg_solver {
   int dev = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t own = nullptr;
-  double2* coef2 = nullptr;  // 4 planes: (b,lam) (w) (bt) (c), n*ntp each
-  double* ath = nullptr;
-  double* cot = nullptr;
-  double2* reg[5] = {};      // state registers: psi plane then pi plane
+  double2* coef = nullptr;   // coefficient blocks (row, chunk) x 144 double2
+  double* cot = nullptr;     // cot(theta), padded to nchunks*32
+  double2* reg[5] = {};      // state registers, blocked layout incl. halo rows
   int nreg = 0;
-  size_t plane = 0;          // (n + 2 kHalo) * ntp double2 per plane
+  size_t rs = 0;             // double2 per state row (nchunks * 64)
+  size_t reg_elems = 0;      // double2 per register ((n + 2 kHalo) * rs)
   int cur = 0, scr1 = 1, scr2 = 2, scr3 = 3, scr4 = 4;
   unsigned long long* flag = nullptr;
   unsigned long long* hflag = nullptr;  // pinned
@@ -110,12 +110,13 @@ struct hwg_solver {
 namespace hwg {
 
 __global__ void relayout_kernel(const double* __restrict__ src, double* __restrict__ dst,
-                                double2* psi, double2* pi, int n, int nt, int ntp, int stride,
-                                int dir) {
+                                double2* reg, int n, int nt, int nchunks, int stride, int dir) {
+  // reg points at row 0 of a blocked state register
   __shared__ double tile[4][32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const size_t W = (size_t)n + 8, Hh = (size_t)nt + 4, P = W * Hh;
+  const size_t rs = (size_t)nchunks * kStateBlk;
   if (dir == 0) {
     for (int kk = ty; kk < 32; kk += 8) {
       const int k = k0 + kk, j = j0 + tx;
@@ -127,19 +128,19 @@ __global__ void relayout_kernel(const double* __restrict__ src, double* __restri
     for (int jj = ty; jj < 32; jj += 8) {
       const int j = j0 + jj, k = k0 + tx;
       if (k < nt && j < n) {
-        const size_t o = (size_t)j * ntp + k;
-        psi[o] = make_double2(tile[0][tx][jj], tile[1][tx][jj]);
-        pi[o] = make_double2(tile[2][tx][jj], tile[3][tx][jj]);
+        double2* b = reg + j * rs + (size_t)(k >> 5) * kStateBlk + (k & 31);
+        b[0] = make_double2(tile[0][tx][jj], tile[1][tx][jj]);
+        b[32] = make_double2(tile[2][tx][jj], tile[3][tx][jj]);
       }
     }
   } else {
     for (int jj = ty; jj < 32; jj += 8) {
       const int j = j0 + jj, k = k0 + tx;
       if (k < nt && j < n) {
-        const size_t o = (size_t)j * ntp + k;
-        double2 a = psi[o], b = pi[o];
-        tile[0][tx][jj] = a.x; tile[1][tx][jj] = a.y;
-        tile[2][tx][jj] = b.x; tile[3][tx][jj] = b.y;
+        const double2* b = reg + j * rs + (size_t)(k >> 5) * kStateBlk + (k & 31);
+        double2 u = b[0], v = b[32];
+        tile[0][tx][jj] = u.x; tile[1][tx][jj] = u.y;
+        tile[2][tx][jj] = v.x; tile[3][tx][jj] = v.y;
       }
     }
     __syncthreads();
@@ -155,9 +156,9 @@ __global__ void relayout_kernel(const double* __restrict__ src, double* __restri
   }
 }
 
-// coefficient plane (index j + ld*k) -> device member (row j, column k)
-__global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, double* dst,
-                            int dst_stride, int n, int nt, int ntp) {
+// coefficient plane q (index j + ld*k, rows row0..) -> blocked coefficient member
+__global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, double* coef,
+                            int q, int n, int nt, int nchunks) {
   __shared__ double tile[32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -168,12 +169,21 @@ __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, do
   __syncthreads();
   for (int jj = ty; jj < 32; jj += 8) {
     const int j = j0 + jj, k = k0 + tx;
-    if (j < n && k < ntp) dst[((size_t)j * ntp + k) * dst_stride] = (k < nt) ? tile[tx][jj] : 0.0;
+    if (j < n && k < nchunks * 32) {
+      const size_t blk = ((size_t)j * nchunks + (k >> 5)) * kCoefBlk;  // double2 units
+      size_t o;
+      if (q < 8) o = (blk + (q / 2) * 32 + (k & 31)) * 2 + (q % 2);
+      else o = (blk + kCoefAth) * 2 + (k & 31);
+      coef[o] = (k < nt) ? tile[tx][jj] : 0.0;
+    }
   }
 }
 
-__global__ void observe_kernel(const double2* psi, int ntp, int j0, const double* hw, int kobs,
-                               int jobs, int jscri, const double* pw, int nt, double* out) {
+__global__ void observe_kernel(const double2* reg, int nchunks, int j0, const double* hw,
+                               int kobs, int jobs, int jscri, const double* pw, int nt,
+                               double* out) {
+  const size_t rs = (size_t)nchunks * kStateBlk;
+  auto psi = [&](int j, int k) { return reg[j * rs + (size_t)(k >> 5) * kStateBlk + (k & 31)]; };
   const int lane = threadIdx.x;
   if (lane == 0) {
     // HorizonSampler::sample (diagnostics.cpp:145-160): sequential dot products
@@ -181,23 +191,23 @@ __global__ void observe_kernel(const double2* psi, int ntp, int j0, const double
       double sr = 0.0, si = 0.0;
       if (j0 >= 0 && kobs >= 0)
         for (int i = 0; i < 5 + d; ++i) {
-          const double2 v = psi[(size_t)(j0 + i) * ntp + kobs];
+          const double2 v = psi(j0 + i, kobs);
           sr = sr + hw[d * 8 + i] * v.x;
           si = si + hw[d * 8 + i] * v.y;
         }
       out[2 * d] = sr;
       out[2 * d + 1] = si;
     }
-    double2 o = (jobs >= 0 && kobs >= 0) ? psi[(size_t)jobs * ntp + kobs] : make_double2(0, 0);
+    double2 o = (jobs >= 0 && kobs >= 0) ? psi(jobs, kobs) : make_double2(0, 0);
     out[8] = o.x; out[9] = o.y;
-    double2 sc = (jscri >= 0 && kobs >= 0) ? psi[(size_t)jscri * ntp + kobs] : make_double2(0, 0);
+    double2 sc = (jscri >= 0 && kobs >= 0) ? psi(jscri, kobs) : make_double2(0, 0);
     out[10] = sc.x; out[11] = sc.y;
   }
   // multipole_project as a linear functional of the theta slice at jobs
   double pr = 0.0, pim = 0.0;
   if (jobs >= 0)
     for (int k = lane; k < nt; k += 32) {
-      const double2 v = psi[(size_t)jobs * ntp + k];
+      const double2 v = psi(jobs, k);
       pr = fma(pw[k], v.x, pr);
       pim = fma(pw[k], v.y, pim);
     }
@@ -231,6 +241,7 @@ void launch_m(const hwg_solver* s, const StageArgs& a, int epi) {
     case EPI_RHS: launch_t<SCH, MODE, EPI_RHS>(s, a); break;
     case EPI_AXPY: launch_t<SCH, MODE, EPI_AXPY>(s, a); break;
     case EPI_RK3: launch_t<SCH, MODE, EPI_RK3>(s, a); break;
+    case EPI_RK3C: launch_t<SCH, MODE, EPI_RK3C>(s, a); break;
     case EPI_RK104_5: launch_t<SCH, MODE, EPI_RK104_5>(s, a); break;
     default: launch_t<SCH, MODE, EPI_RK104_10>(s, a); break;
   }
@@ -238,8 +249,13 @@ void launch_m(const hwg_solver* s, const StageArgs& a, int epi) {
 
 template <int SCH>
 void launch_s(const hwg_solver* s, const StageArgs& a, int epi) {
-  if (s->d.precision == HWG_F64) launch_m<SCH, F64>(s, a, epi);
-  else launch_m<SCH, MIXED>(s, a, epi);
+  if constexpr (SCH == FD6KO) {
+    launch_m<SCH, F64>(s, a, epi);  // no weights
+  } else {
+    if (std::isinf(s->d.eps)) launch_m<SCH, LIN>(s, a, epi);
+    else if (s->d.precision == HWG_F64) launch_m<SCH, F64>(s, a, epi);
+    else launch_m<SCH, MIXED>(s, a, epi);
+  }
 }
 
 int launch(hwg_solver* s, const StageArgs& a, int epi) {
@@ -256,15 +272,14 @@ int launch(hwg_solver* s, const StageArgs& a, int epi) {
   return HWG_OK;
 }
 
-double2* psi_of(const hwg_solver* s, int r) { return s->reg[r] + (size_t)kHalo * s->ntp; }
-double2* pi_of(const hwg_solver* s, int r) { return s->reg[r] + s->plane + (size_t)kHalo * s->ntp; }
+// row-0 pointer of state register r
+double2* row0(const hwg_solver* s, int r) { return s->reg[r] + (size_t)kHalo * s->rs; }
 
 StageArgs base_args(const hwg_solver* s) {
   StageArgs a{};
-  a.n = s->n; a.nt = s->nt; a.ntp = s->ntp;
+  a.n = s->n; a.nt = s->nt; a.nchunks = s->nchunks;
   a.phys_lo = s->phys_lo; a.phys_hi = s->phys_hi;
-  a.nchunks = s->nchunks; a.nranges = s->nranges;
-  a.linear = std::isinf(s->d.eps) ? 1 : 0;
+  a.nranges = s->nranges;
   a.negpar = s->d.parity < 0 ? 1 : 0;
   a.eps4 = 4.0 * s->d.eps;
   a.eps = s->d.eps;
@@ -276,26 +291,22 @@ StageArgs base_args(const hwg_solver* s) {
   a.inv1 = 1.0 / (12.0 * s->d.dtheta);
   a.inv2 = 1.0 / (12.0 * s->d.dtheta * s->d.dtheta);
   a.ko = s->d.sigma / (256.0 * dr);
-  a.cbl = s->coef2;
-  a.cw = s->coef2 + (size_t)s->n * s->ntp;
-  a.cbt = s->coef2 + 2 * (size_t)s->n * s->ntp;
-  a.ccf = s->coef2 + 3 * (size_t)s->n * s->ntp;
-  a.cath = s->ath;
+  a.coef = s->coef;
   a.cot = s->cot;
   a.flag = s->flag;
   return a;
 }
 
 void set_io(StageArgs& a, const hwg_solver* s, int x, int out) {
-  a.xpsi = psi_of(s, x); a.xpi = pi_of(s, x);
-  a.opsi = psi_of(s, out); a.opi = pi_of(s, out);
+  a.x = row0(s, x);
+  a.o = row0(s, out);
 }
 
 int ensure_regs(hwg_solver* s, int need) {
   while (s->nreg < need) {
     double2* p = nullptr;
-    CK(cudaMalloc(&p, 2 * s->plane * sizeof(double2)));
-    CK(cudaMemsetAsync(p, 0, 2 * s->plane * sizeof(double2), s->stream));
+    CK(cudaMalloc(&p, s->reg_elems * sizeof(double2)));
+    CK(cudaMemsetAsync(p, 0, s->reg_elems * sizeof(double2), s->stream));
     s->reg[s->nreg++] = p;
   }
   return HWG_OK;
@@ -324,7 +335,7 @@ int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, 
       a.cg = dt;
       return launch(s, a, EPI_AXPY);
     }
-    a.apsi = psi_of(s, s->cur); a.api = pi_of(s, s->cur);
+    a.ua = row0(s, s->cur);
     a.cg = dt;
     if (stage == 1) {
       set_io(a, s, s->scr1, s->scr2);
@@ -333,8 +344,7 @@ int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, 
     }
     set_io(a, s, s->scr2, s->scr1);
     a.ca = ddq(1.0, 3.0); a.cb = ddq(2.0, 3.0);
-    a.check = 1;
-    int rc = launch(s, a, EPI_RK3);
+    int rc = launch(s, a, EPI_RK3C);
     std::swap(s->cur, s->scr1);
     return rc;
   }
@@ -346,19 +356,18 @@ int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, 
   const int outs[10] = {P, Q, P, S4, P, Q, P, Q, P, Q};
   set_io(a, s, ins[stage], outs[stage]);
   if (stage == 4) {
-    a.apsi = psi_of(s, U); a.api = pi_of(s, U);
-    a.fpsi = psi_of(s, F4); a.fpi = pi_of(s, F4);
+    a.ua = row0(s, U);
+    a.f = row0(s, F4);
     a.ca = ddq(3.0, 5.0); a.cb = ddq(2.0, 5.0);
     a.cg = dd_div(dtd, {15.0, 0.0}).hi;
     return launch(s, a, EPI_RK104_5);
   }
   if (stage == 9) {
-    a.apsi = psi_of(s, U); a.api = pi_of(s, U);
-    a.bpsi = psi_of(s, S4); a.bpi = pi_of(s, S4);
-    a.gpsi = psi_of(s, F4); a.gpi = pi_of(s, F4);
+    a.ua = row0(s, U);
+    a.ub = row0(s, S4);
+    a.ug = row0(s, F4);
     a.ca = ddq(1.0, 25.0); a.cb = ddq(9.0, 25.0); a.cc = ddq(3.0, 5.0);
     a.cg = dt; a.cd = ddq(3.0, 50.0); a.ce = ddq(1.0, 10.0);
-    a.check = 1;
     int rc = launch(s, a, EPI_RK104_10);
     std::swap(s->cur, s->scr2);
     return rc;
@@ -378,8 +387,8 @@ int upload_layout(hwg_solver* s, const double* host, int stride, int reg) {
   }
   CK(cudaMemcpyAsync(s->stage_dev, host, cnt * sizeof(double), cudaMemcpyHostToDevice, s->stream));
   dim3 grid((s->n + 31) / 32, (s->nt + 31) / 32), blk(32, 8);
-  relayout_kernel<<<grid, blk, 0, s->stream>>>(s->stage_dev, nullptr, psi_of(s, reg),
-                                                pi_of(s, reg), s->n, s->nt, s->ntp, stride, 0);
+  relayout_kernel<<<grid, blk, 0, s->stream>>>(s->stage_dev, nullptr, row0(s, reg), s->n, s->nt,
+                                                s->nchunks, stride, 0);
   CK(cudaGetLastError());
   return HWG_OK;
 }
@@ -397,8 +406,8 @@ int download_layout(hwg_solver* s, double* host, int stride, int reg, bool ghost
   }
   CK(cudaMemsetAsync(s->stage_dev, 0, cnt * sizeof(double), s->stream));
   dim3 grid((s->n + 31) / 32, (s->nt + 31) / 32), blk(32, 8);
-  relayout_kernel<<<grid, blk, 0, s->stream>>>(nullptr, s->stage_dev, psi_of(s, reg),
-                                                pi_of(s, reg), s->n, s->nt, s->ntp, stride, 1);
+  relayout_kernel<<<grid, blk, 0, s->stream>>>(nullptr, s->stage_dev, row0(s, reg), s->n, s->nt,
+                                                s->nchunks, stride, 1);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(host, s->stage_dev, cnt * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
@@ -534,10 +543,12 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
   s->n = d->nrho;
   s->nt = d->ntheta;
   s->ntp = (d->ntheta + 31) / 32 * 32;
+  s->nchunks = s->ntp / 32;
+  s->rs = (size_t)s->nchunks * kStateBlk;
   s->phys_lo = d->rho_offset == 0;
   s->phys_hi = d->rho_offset + d->nrho == nglob;
   s->dev = d->device;
-  s->plane = (size_t)(s->n + 2 * kHalo) * s->ntp;
+  s->reg_elems = (size_t)(s->n + 2 * kHalo) * s->rs;
   auto fail = [&](int rc) {
     g_create_err = s->err;
     hwg_destroy(s);
@@ -558,9 +569,9 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
   } while (0)
   CK(cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking));
   s->stream = s->own;
-  const size_t P = (size_t)s->n * s->ntp;
-  CK(cudaMalloc(&s->coef2, 4 * P * sizeof(double2)));
-  CK(cudaMalloc(&s->ath, P * sizeof(double)));
+  const size_t CB = (size_t)s->n * s->nchunks * kCoefBlk;
+  CK(cudaMalloc(&s->coef, CB * sizeof(double2)));
+  CK(cudaMemsetAsync(s->coef, 0, CB * sizeof(double2), s->stream));
   CK(cudaMalloc(&s->cot, s->ntp * sizeof(double)));
   CK(cudaMalloc(&s->flag, 2 * sizeof(unsigned long long)));
   CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
@@ -575,15 +586,12 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
     double* tmp = nullptr;
     const size_t plane_src = (size_t)ld * s->nt;
     CK(cudaMalloc(&tmp, plane_src * sizeof(double)));
-    dim3 grid((s->n + 31) / 32, (s->ntp + 31) / 32), blk(32, 8);
+    dim3 grid((s->n + 31) / 32, s->nchunks), blk(32, 8);
     for (int q = 0; q < 9; ++q) {
       CK(cudaMemcpyAsync(tmp, coef + q * plane_src, plane_src * sizeof(double),
                          cudaMemcpyHostToDevice, s->stream));
-      double* dst;
-      int stride;
-      if (q == 8) { dst = s->ath; stride = 1; }
-      else { dst = reinterpret_cast<double*>(s->coef2 + (q / 2) * P) + (q % 2); stride = 2; }
-      coef_kernel<<<grid, blk, 0, s->stream>>>(tmp, ld, row0, dst, stride, s->n, s->nt, s->ntp);
+      coef_kernel<<<grid, blk, 0, s->stream>>>(tmp, ld, row0, reinterpret_cast<double*>(s->coef), q,
+                                                s->n, s->nt, s->nchunks);
       CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(s->stream));
@@ -593,7 +601,7 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
     CK(cudaMemcpy(s->cot, c.data(), s->ntp * sizeof(double), cudaMemcpyHostToDevice));
   }
   {
-    int rc = ensure_regs(s, d->scheme == HWG_FD6KO || true ? 3 : 3);
+    int rc = ensure_regs(s, 3);
     if (rc) return fail(rc);
   }
   // launch geometry: one wave of warps, rho ranges balanced per theta chunk
@@ -608,7 +616,6 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_kernel<WENO5, F64, EPI_RK3>,
                                                      kWarpsPerBlock * 32,
                                                      stage_smem_bytes<EPI_RK3>()));
-    s->nchunks = s->ntp / 32;
     const long long target = (long long)nsm * std::max(occ, 1) * kWarpsPerBlock;
     long long nr = std::max<long long>(1, target / s->nchunks);
     nr = std::min<long long>(nr, std::max(1, s->n / 8));  // >= 8 rows per range
@@ -634,8 +641,7 @@ void hwg_destroy(hwg_solver* s) {
   cudaSetDevice(s->dev);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (int i = 0; i < s->nreg; ++i) cudaFree(s->reg[i]);
-  cudaFree(s->coef2);
-  cudaFree(s->ath);
+  cudaFree(s->coef);
   cudaFree(s->cot);
   cudaFree(s->flag);
   cudaFree(s->stage_dev);
@@ -716,11 +722,10 @@ int hwg_stage_input(const hwg_solver* s, int stepper, int stage, int* reg) {
   return HWG_OK;
 }
 
-int hwg_register_planes(const hwg_solver* s, int reg, void** psi, void** pi, int* pitch) {
+int hwg_register_ptr(const hwg_solver* s, int reg, void** row0_ptr, long long* row_elems) {
   if (reg < 0 || reg >= s->nreg) return HWG_EINVAL;
-  *psi = psi_of(s, reg);
-  *pi = pi_of(s, reg);
-  *pitch = s->ntp;
+  *row0_ptr = row0(s, reg);
+  *row_elems = (long long)s->rs;
   return HWG_OK;
 }
 
@@ -742,7 +747,7 @@ int hwg_launch_info(const hwg_solver* s, int* blocks, int* threads, int* nranges
   *threads = kWarpsPerBlock * 32;
   *nranges = s->nranges;
   *nchunks = s->nchunks;
-  *pitch = s->ntp;
+  *pitch = (int)s->rs;
   return HWG_OK;
 }
 
@@ -768,7 +773,7 @@ int hwg_set_observers(hwg_solver* s, int kobs, int j0, const double* hw, int job
 }
 
 int hwg_observe(hwg_solver* s, hwg_observables* out) {
-  observe_kernel<<<1, 32, 0, s->stream>>>(psi_of(s, s->cur), s->ntp, s->j0, s->obs_w, s->kobs,
+  observe_kernel<<<1, 32, 0, s->stream>>>(row0(s, s->cur), s->nchunks, s->j0, s->obs_w, s->kobs,
                                            s->jobs, s->phys_hi ? s->n - 1 : -1, s->obs_w + 32,
                                            s->nt, s->obs_dev);
   CK(cudaGetLastError());

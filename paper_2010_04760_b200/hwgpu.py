@@ -77,8 +77,7 @@ _lib.hwg_observe.argtypes = [_vp, C.POINTER(HwgObservables)]
 _lib.hwg_launch_stage.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_longlong]
 _lib.hwg_launch_steps.argtypes = [_vp, C.c_int, C.c_double, C.c_double, C.c_longlong, C.c_longlong]
 _lib.hwg_stage_input.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(C.c_int)]
-_lib.hwg_register_planes.argtypes = [_vp, C.c_int, C.POINTER(_vp), C.POINTER(_vp),
-                                     C.POINTER(C.c_int)]
+_lib.hwg_register_ptr.argtypes = [_vp, C.c_int, C.POINTER(_vp), C.POINTER(C.c_longlong)]
 _lib.hwg_current_register.argtypes = [_vp]
 _lib.hwg_status.argtypes = [_vp, C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.c_int]
 _lib.hwg_launch_info.argtypes = [_vp] + [C.POINTER(C.c_int)] * 5
@@ -87,7 +86,7 @@ _lib.hwg_synchronize.argtypes = [_vp]
 EXPORTED = ["hwg_create", "hwg_destroy", "hwg_last_error", "hwg_set_stream", "hwg_set_state_dd",
             "hwg_get_state_dd", "hwg_set_state", "hwg_get_state", "hwg_rhs", "hwg_rhs_dd",
             "hwg_advance", "hwg_set_observers", "hwg_observe", "hwg_launch_stage",
-            "hwg_launch_steps", "hwg_stage_input", "hwg_register_planes",
+            "hwg_launch_steps", "hwg_stage_input", "hwg_register_ptr",
             "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize"]
 
 
@@ -252,23 +251,20 @@ class GpuEvolution:
     def current_register(self) -> int:
         return _lib.hwg_current_register(self.h)
 
-    def register_planes(self, reg: int):
-        """(psi_row0_ptr, pi_row0_ptr, row_pitch) of a state register."""
-        a, b, p = _vp(), _vp(), C.c_int()
-        self._chk(_lib.hwg_register_planes(self.h, reg, C.byref(a), C.byref(b), C.byref(p)))
-        return a.value, b.value, p.value
+    def register_ptr(self, reg: int):
+        """(row-0 device pointer, double2 per row) of a state register."""
+        a, r = _vp(), C.c_longlong()
+        self._chk(_lib.hwg_register_ptr(self.h, reg, C.byref(a), C.byref(r)))
+        return a.value, r.value
 
-    def register_views(self, reg: int):
-        """torch views (rows -4..nrho+3, pitch, 2) of a register's psi and pi planes."""
+    def register_view(self, reg: int):
+        """torch view (nrho + 8 rows, row doubles) of a state register, halo rows
+        included (row index 4 is grid row 0).  A row is contiguous: 32-column
+        blocks [Psi(32) | pi(32)] of (re, im) pairs."""
         import torch
-        ps, pi, pitch = self.register_planes(reg)
+        ptr, row = self.register_ptr(reg)
         rows = self.nrho + 2 * HALO
-        off = HALO * pitch * 16
-        views = []
-        for ptr in (ps, pi):
-            t = torch.as_tensor(_DevArray(ptr - off, (rows, pitch, 2)), device="cuda")
-            views.append(t)
-        return views
+        return torch.as_tensor(_DevArray(ptr - HALO * row * 16, (rows, 2 * row)), device="cuda")
 
     def status(self, clear: bool = False):
         b, s = C.c_int(), C.c_longlong()

@@ -33,16 +33,12 @@ def partition(nrho_global: int, world: int):
 
 
 def halo_views(backend, reg: int, h: int):
-    """(send_left, recv_left, send_right, recv_right) views of both planes of
-    register `reg`; each is a list [psi_view, pi_view]."""
-    ps, pi = backend.register_views(reg)
+    """(send_left, recv_left, send_right, recv_right) row views of register
+    `reg` (a row is contiguous, so each is one contiguous message)."""
+    v = backend.register_view(reg)
     n = backend.nrho
     H = BUF_HALO
-    sl = [p[H:H + h] for p in (ps, pi)]                  # my rows 0..h-1
-    rl = [p[H - h:H] for p in (ps, pi)]                  # rows -h..-1
-    sr = [p[H + n - h:H + n] for p in (ps, pi)]          # my rows n-h..n-1
-    rr = [p[H + n:H + n + h] for p in (ps, pi)]          # rows n..n+h-1
-    return sl, rl, sr, rr
+    return v[H:H + h], v[H - h:H], v[H + n - h:H + n], v[H + n:H + n + h]
 
 
 class DistSlab:
@@ -62,13 +58,12 @@ class DistSlab:
             return
         sl, rl, sr, rr = halo_views(self.b, reg, self.h)
         ops = []
-        for i in range(2):
-            if self.left is not None:
-                ops.append(dist.P2POp(dist.isend, sl[i].contiguous() if not sl[i].is_contiguous() else sl[i], self.left, self.group))
-                ops.append(dist.P2POp(dist.irecv, rl[i], self.left, self.group))
-            if self.right is not None:
-                ops.append(dist.P2POp(dist.isend, sr[i], self.right, self.group))
-                ops.append(dist.P2POp(dist.irecv, rr[i], self.right, self.group))
+        if self.left is not None:
+            ops.append(dist.P2POp(dist.isend, sl, self.left, self.group))
+            ops.append(dist.P2POp(dist.irecv, rl, self.left, self.group))
+        if self.right is not None:
+            ops.append(dist.P2POp(dist.isend, sr, self.right, self.group))
+            ops.append(dist.P2POp(dist.irecv, rr, self.right, self.group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
 
@@ -93,12 +88,10 @@ class LocalSlabs:
     def exchange(self, regs):
         views = [halo_views(b, r, self.h) for b, r in zip(self.bs, regs)]
         for i in range(len(self.bs) - 1):
-            _, _, sr, _ = views[i]
+            _, _, sr, rr = views[i]
             sl, rl, _, _ = views[i + 1]
-            _, _, _, rr = views[i]
-            for p in range(2):
-                rl[p].copy_(sr[p])   # right neighbour's left halo <- my last rows
-                rr[p].copy_(sl[p])   # my right halo <- right neighbour's first rows
+            rl.copy_(sr)   # right neighbour's left halo <- my last rows
+            rr.copy_(sl)   # my right halo <- right neighbour's first rows
 
     def step(self, stepper: str, dt, step: int):
         ns = 3 if stepper == "ssprk33" else 10
