@@ -1,0 +1,137 @@
+// hweno_gpu_dropin.hpp — header-only C++ drop-in for the reference solver.
+//
+// A reference maintainer includes this next to the reference's own headers
+// (proj/include/hweno/*.hpp) and links libhwgpu.so.  It keeps the reference's
+// types and call shapes, so driver code (proj/src/driver.cpp:22-137,
+// proj/tools/main.cpp:168-221) changes only in the two lines that construct
+// the RHS and call the time loop:
+//
+//   hweno::EvolutionRhs rhs(g, cs, p, spec, pool);            // reference
+//   hweno_gpu::GpuEvolutionRhs rhs(g, cs, p, spec);           // GPU
+//
+//   advance_steps(rhs, stepper, u, dt, 0, n, hook, pool);      // reference
+//   hweno_gpu::advance_steps(rhs, stepper, u, dt, 0, n, hook); // GPU
+//
+// Semantics follow proj/src/evolve.cpp:10-265: operator() fills u's ghosts and
+// writes du's interior; advance_steps fires the hook at s % every == 0, at the
+// first and at the last step (with tau = s * dt in double-double), stops at
+// the first inadmissible state and reports RunStats.  The GPU tiers are one
+// below the reference's: SchemeSpec::mode full -> HWG_F64,
+// mixed -> HWG_MIXED (fp32 weights).  Errors surface as the reference's
+// exception types.
+#pragma once
+
+#include <chrono>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hweno/evolve.hpp"
+#include "hweno/geometry.hpp"
+#include "hweno/timestep.hpp"
+#include "hweno_gpu.h"
+
+namespace hweno_gpu {
+
+inline void check(int rc, const hwg_solver* s) {
+  if (rc == HWG_OK) return;
+  std::string msg = hwg_last_error(s);
+  if (rc == HWG_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+class GpuEvolutionRhs {
+ public:
+  GpuEvolutionRhs(const hweno::Grid& g, const hweno::CoefficientSet& cs,
+                  const hweno::PhysicalParams& p, const hweno::SchemeSpec& spec,
+                  int device = 0)
+      : lay_{g.nrho, g.ntheta}, spec_(spec) {
+    const size_t P = size_t(g.nrho) * g.ntheta;
+    const std::vector<hweno::WorkReal>* src[9] = {&cs.b,     &cs.lam,   &cs.w_re,
+                                                  &cs.w_im,  &cs.bt_re, &cs.bt_im,
+                                                  &cs.c_re,  &cs.c_im,  &cs.ath};
+    std::vector<double> planes(9 * P), cot(g.ntheta);
+    for (int q = 0; q < 9; ++q)
+      for (size_t i = 0; i < P; ++i) planes[q * P + i] = (*src[q])[i].hi;
+    for (int k = 0; k < g.ntheta; ++k) cot[k] = cs.cotth[k].hi;
+    hwg_desc d{};
+    d.nrho = g.nrho;
+    d.ntheta = g.ntheta;
+    d.drho = g.drho.hi;
+    d.dtheta = g.dtheta.hi;
+    d.parity = ((p.mmode + p.spin) % 2 == 0) ? 1 : -1;  // evolve.cpp:18
+    d.scheme = spec.scheme == hweno::Scheme::weno5   ? HWG_WENO5
+               : spec.scheme == hweno::Scheme::weno3 ? HWG_WENO3
+                                                     : HWG_FD6KO;
+    d.precision = spec.mode == hweno::PrecisionMode::full ? HWG_F64 : HWG_MIXED;
+    d.eps = spec.eps.hi;
+    d.sigma = spec.sigma.hi;
+    d.device = device;
+    d.rho_offset = 0;
+    d.nrho_global = g.nrho;
+    d.coef_ld = g.nrho;
+    d.coef_row0 = 0;
+    check(hwg_create(&d, planes.data(), cot.data(), &h_), nullptr);
+  }
+  ~GpuEvolutionRhs() { hwg_destroy(h_); }
+  GpuEvolutionRhs(const GpuEvolutionRhs&) = delete;
+  GpuEvolutionRhs& operator=(const GpuEvolutionRhs&) = delete;
+
+  // EvolutionRhs::operator() (evolve.hpp:61): DDReal is {double hi, lo}
+  void operator()(hweno::StateVec& u, hweno::StateVec& du) {
+    check(hwg_rhs_dd(h_, reinterpret_cast<double*>(u.data()),
+                     reinterpret_cast<double*>(du.data())),
+          h_);
+  }
+
+  const hweno::FieldLayout& layout() const { return lay_; }
+  const hweno::SchemeSpec& scheme() const { return spec_; }
+  hwg_solver* handle() { return h_; }
+
+ private:
+  hweno::FieldLayout lay_;
+  hweno::SchemeSpec spec_;
+  hwg_solver* h_ = nullptr;
+};
+
+namespace detail {
+struct HookCtx {
+  GpuEvolutionRhs* rhs;
+  const hweno::SampleHook* hook;
+  hweno::StateVec* u;
+};
+inline void trampoline(long long step, double tau_hi, double tau_lo, const hwg_observables*,
+                       void* user) {
+  auto* c = static_cast<HookCtx*>(user);
+  // the reference hook sees the full state (driver.cpp:64-91): bring it back
+  check(hwg_get_state_dd(c->rhs->handle(), reinterpret_cast<double*>(c->u->data())),
+        c->rhs->handle());
+  c->hook->fn(long(step), hweno::WorkReal(tau_hi, tau_lo), *c->u);
+}
+}  // namespace detail
+
+// advance_steps (evolve.hpp:109-112) on the GPU.  u is uploaded once, stays
+// on the device for the whole call and is written back at the end (and at
+// hook steps, for the hook).
+inline hweno::RunStats advance_steps(GpuEvolutionRhs& rhs, const hweno::StepperSpec& stepper,
+                                     hweno::StateVec& u, const hweno::WorkReal& dt,
+                                     long step_begin, long step_end,
+                                     const hweno::SampleHook& hook) {
+  hwg_solver* h = rhs.handle();
+  check(hwg_set_state_dd(h, reinterpret_cast<const double*>(u.data())), h);
+  detail::HookCtx ctx{&rhs, &hook, &u};
+  hwg_run_stats st{};
+  const int kind = stepper.kind == hweno::StepperSpec::ssprk33 ? HWG_SSPRK33 : HWG_SSPRK104;
+  check(hwg_advance(h, kind, dt.hi, dt.lo, step_begin, step_end, hook.fn ? hook.every : 1,
+                    hook.fn ? detail::trampoline : nullptr, &ctx, &st),
+        h);
+  check(hwg_get_state_dd(h, reinterpret_cast<double*>(u.data())), h);
+  hweno::RunStats rs;
+  rs.steps_done = long(st.steps_done);
+  rs.wall_seconds = st.wall_seconds;
+  rs.blew_up = st.blew_up != 0;
+  rs.blowup_step = long(st.blowup_step);
+  return rs;
+}
+
+}  // namespace hweno_gpu

@@ -1,0 +1,118 @@
+// TEST INFRASTRUCTURE ONLY — end-to-end check of the C++ drop-in
+// (include/hweno_gpu_dropin.hpp) inside the reference's own setup code.
+//
+// The reference builds the grid, coefficients and initial data
+// (proj/src/geometry.cpp, proj/src/evolve.cpp:189-215) and runs its own
+// advance_steps with a driver-style hook (proj/src/driver.cpp:64-80); the same
+// driver code then runs hweno_gpu::advance_steps.  Exit 0 iff the final states,
+// the hook cadence and the hook's horizon observables agree.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "hweno/diagnostics.hpp"
+#include "hweno/evolve.hpp"
+#include "hweno_gpu_dropin.hpp"
+
+using namespace hweno;
+
+struct Run {
+  std::vector<long> steps;
+  std::vector<double> charge;  // Aretakis charge dphi[0].re
+  StateVec u;
+  RunStats st;
+};
+
+template <class Rhs, class Adv>
+Run drive(Rhs& rhs, const Grid& g, const PhysicalParams& p, StateVec u0, const WorkReal& dt,
+          long nsteps, Adv&& adv) {
+  Run r;
+  HorizonSampler hs(g, p, rhs.layout(), g.ntheta / 2);
+  SampleHook hook;
+  hook.every = 10;
+  hook.fn = [&](long s, const WorkReal&, const StateVec& u) {
+    r.steps.push_back(s);
+    r.charge.push_back(hs.sample(u).dphi[0].re.hi);
+  };
+  r.u = u0;
+  r.st = adv(rhs, r.u, dt, nsteps, hook);
+  return r;
+}
+
+int main(int argc, char** argv) {
+  int device = argc > 1 ? std::atoi(argv[1]) : 0;
+  int bad = 0;
+  for (int mode = 0; mode < 2; ++mode) {
+    PhysicalParams p;
+    p.M = WorkReal(1);
+    p.a = WorkReal(0.9);
+    p.spin = -2;
+    p.mmode = 0;
+    p.S = WorkReal(20);
+    Grid g = make_grid(256, 16, p);
+    CoefficientSet cs = assemble_coefficients(g, p);
+    SchemeSpec spec;
+    spec.mode = mode == 0 ? PrecisionMode::full : PrecisionMode::mixed;
+    InitialDataSpec id;
+    id.center = WorkReal(3.0);
+    id.width = WorkReal(0.3);
+    StateVec u0 = initial_data(g, cs, p, id);
+    StepperSpec st;
+    st.kind = StepperSpec::ssprk104;
+    WorkReal dt = select_dt(g, cs, st);
+    const long nsteps = 45;
+
+    WorkerPool pool(4);
+    EvolutionRhs ref(g, cs, p, spec, pool);
+    Run a = drive(ref, g, p, u0, dt, nsteps,
+                  [&](EvolutionRhs& r, StateVec& u, const WorkReal& d, long n,
+                      const SampleHook& h) {
+                    return advance_steps(r, st, u, d, 0, n, h, pool);
+                  });
+    hweno_gpu::GpuEvolutionRhs gpu(g, cs, p, spec, device);
+    Run b = drive(gpu, g, p, u0, dt, nsteps,
+                  [&](hweno_gpu::GpuEvolutionRhs& r, StateVec& u, const WorkReal& d, long n,
+                      const SampleHook& h) {
+                    return hweno_gpu::advance_steps(r, st, u, d, 0, n, h);
+                  });
+    double num = 0, den = 0;
+    const FieldLayout& lay = ref.layout();
+    for (int c = 0; c < kComponents; ++c)
+      for (int k = 0; k < g.ntheta; ++k)
+        for (int j = 0; j < g.nrho; ++j) {
+          size_t i = lay.at(c, j, k);
+          num = std::fmax(num, std::fabs(a.u[i].hi - b.u[i].hi));
+          den = std::fmax(den, std::fabs(a.u[i].hi));
+        }
+    const double tol = mode == 0 ? 1e-12 : 1e-6;
+    double cerr = 0;
+    for (size_t q = 0; q < a.charge.size() && q < b.charge.size(); ++q)
+      cerr = std::fmax(cerr, std::fabs(a.charge[q] - b.charge[q]) /
+                                 std::fmax(std::fabs(a.charge[q]), 1e-12));
+    const bool ok = a.steps == b.steps && b.st.steps_done == nsteps && !b.st.blew_up &&
+                    num / den <= tol && cerr <= (mode == 0 ? 1e-9 : 1e-4);
+    std::printf("%s: state rel %.3e  hooks %zu/%zu  charge rel %.3e  steps %ld  %s\n",
+                mode == 0 ? "full/f64" : "mixed", num / den, a.steps.size(), b.steps.size(), cerr,
+                b.st.steps_done, ok ? "OK" : "FAIL");
+    bad += !ok;
+
+    // EvolutionRhs::operator() on the same state
+    StateVec u1 = u0, u2 = u0, d1(lay.size()), d2(lay.size());
+    ref(u1, d1);
+    gpu(u2, d2);
+    double rn = 0, rd = 0, gh = 0;
+    for (size_t i = 0; i < lay.size(); ++i) {
+      rn = std::fmax(rn, std::fabs(d1[i].hi - d2[i].hi));
+      rd = std::fmax(rd, std::fabs(d1[i].hi));
+    }
+    for (int c = 0; c < kComponents; ++c)
+      for (int k = 0; k < g.ntheta; ++k)
+        for (int t = 1; t <= kRadialGhost; ++t)
+          gh = std::fmax(gh, std::fabs(u1[lay.at(c, -t, k)].hi - u2[lay.at(c, -t, k)].hi));
+    const bool ok2 = rn / rd <= (mode == 0 ? 1e-13 : 1e-6) && gh <= 1e-13;
+    std::printf("  rhs rel %.3e ghost diff %.3e %s\n", rn / rd, gh, ok2 ? "OK" : "FAIL");
+    bad += !ok2;
+  }
+  std::printf(bad ? "DROPIN FAIL\n" : "DROPIN OK\n");
+  return bad ? 1 : 0;
+}

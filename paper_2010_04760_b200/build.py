@@ -59,6 +59,7 @@ def build_oracle(force: bool = False) -> None:
     subprocess.run(mk + ["oracle"], check=True)
     if os.path.isdir("/root/reference/proj/src"):
         subprocess.run(mk + ["ref", "-j8"], check=True)
+        subprocess.run(mk + ["dropin"], check=True)
 
 
 if __name__ == "__main__":

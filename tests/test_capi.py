@@ -68,3 +68,14 @@ def test_create_validates_like_the_reference():
     coef[1, 0, 5] = 1.0  # lam: - - - - - + - - ... changes sign twice
     with pytest.raises(HwgError, match="more than once"):
         GpuEvolution(16, 4, 0.1, 0.5, 1, coef, np.zeros(4))
+
+
+def test_cpp_dropin_fails_loudly_without_gpu():
+    """No CPU fallback in the C++ drop-in either: without a GPU the reference
+    driver gets an exception (process aborts), never a silent CPU run."""
+    import torch
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_check")
+    if torch.cuda.is_available() or not os.path.exists(exe):
+        pytest.skip("GPU present or drop-in check not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "DROPIN OK" not in r.stdout

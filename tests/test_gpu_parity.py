@@ -241,3 +241,16 @@ def test_radial_slabs_bit_identical(cuda_ok, case, nslabs):
         for off, cnt, h in slabs:
             got = h.get_state()
             np.testing.assert_array_equal(got[:, 2:-2, 4:-4], ref[:, 2:-2, 4 + off:4 + off + cnt])
+
+
+def test_cpp_dropin_inside_reference_driver(cuda_ok):
+    """include/hweno_gpu_dropin.hpp used by reference-style driver code
+    (oracle/dropin_check.cpp, built against the unmodified reference library):
+    GPU advance_steps with a HorizonSampler hook vs the reference's own."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(GOLDEN), "..", "oracle", "_ref", "dropin_check")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in check not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "DROPIN OK" in r.stdout, r.stdout + r.stderr
