@@ -61,6 +61,7 @@ def ref_lib():
         lib.ref_destroy.argtypes = [C.c_void_p]
         lib.ref_info.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_longlong)]
         lib.ref_coeffs.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp]
+        lib.ref_cotth_lo.argtypes = [C.c_void_p, _dp]
         lib.ref_initial_data.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double,
                                          C.c_double, _dp]
         lib.ref_rhs.argtypes = [C.c_void_p, _dp, _dp]
@@ -159,7 +160,7 @@ class RefSolver:
         ints = (C.c_longlong * 5)()
         _chk(lib.ref_info(h, _ptr(d), _ptr(dlo), ints))
         self.drho, self.dtheta, self.rho_min, self.max_speed, self.horizon_rho, _ = d
-        self.drho_lo = dlo[0]
+        self.drho_lo, self.dtheta_lo = dlo[0], dlo[1]
         self.parity = int(ints[2])
         self.horizon_index = int(ints[3])
         self.state_size = int(ints[4])
@@ -171,6 +172,8 @@ class RefSolver:
         self.theta = np.zeros(ntheta)
         _chk(lib.ref_coeffs(h, _ptr(self.coef), _ptr(self.coef_lo), _ptr(self.cotth),
                             _ptr(self.rho), _ptr(self.theta)))
+        self.cotth_lo = np.zeros(ntheta)
+        _chk(lib.ref_cotth_lo(h, _ptr(self.cotth_lo)))
 
     def __del__(self):
         try:

@@ -148,6 +148,14 @@ int ref_coeffs(void* hv, double* planes, double* lo, double* cotth,
   });
 }
 
+// low limbs of cot(theta_k) (CoefficientSet::cotth)
+int ref_cotth_lo(void* hv, double* lo) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    for (int k = 0; k < h->g.ntheta; ++k) lo[k] = h->cs.cotth[k].lo;
+  });
+}
+
 // u_dd: 2*state_size doubles ({hi, lo} pairs, reference FieldLayout)
 int ref_initial_data(void* hv, int ell, double center, double width,
                      double amplitude, double* u_dd) {

@@ -13,9 +13,13 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SO = os.path.join(PKG, "libhwgpu.so")
-SRCS = [os.path.join(PKG, "csrc", "hwg_solver.cu")]
-DEPS = SRCS + [os.path.join(PKG, "csrc", "hwg_kernels.cuh"),
-               os.path.join(ROOT, "include", "hweno_gpu.h")]
+CSRC = os.path.join(PKG, "csrc")
+SRCS = [os.path.join(CSRC, f) for f in ("hwg_solver.cu", "hwg_stage_fast.cu", "hwg_stage_dd.cu")]
+HDRS = [os.path.join(CSRC, f) for f in ("hwg_kernels.cuh", "hwg_dd.cuh", "hwg_launch.h",
+                                        "hwg_dispatch.cuh")] + [
+    os.path.join(ROOT, "include", "hweno_gpu.h")]
+DEPS = SRCS + HDRS
+OBJDIR = os.path.join(PKG, "_obj")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -23,7 +27,7 @@ NVCC_FLAGS = [
     # every multiply-add in the kernels is an explicit fma(): results do not
     # depend on inlining / contraction choices (slab bit-identity)
     "-fmad=false",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC,-ffp-contract=off",
 ]
 
 
@@ -42,11 +46,23 @@ def _stale(target: str, deps) -> bool:
 
 
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
-    if force or _stale(SO, DEPS):
-        cmd = [nvcc(), *NVCC_FLAGS, "-o", SO, *SRCS]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True)
+    """Compile each translation unit (in parallel) and link libhwgpu.so."""
+    os.makedirs(OBJDIR, exist_ok=True)
+    procs, objs = [], []
+    for src in SRCS:
+        obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [src] + HDRS):
+            cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj, src]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            procs.append((src, subprocess.Popen(cmd)))
+    for src, p in procs:
+        if p.wait() != 0:
+            raise RuntimeError(f"nvcc failed on {src}")
+    if force or _stale(SO, objs):
+        subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                        "-o", SO, *objs], check=True)
     return SO
 
 

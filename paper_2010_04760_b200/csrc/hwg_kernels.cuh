@@ -107,7 +107,7 @@ __device__ __forceinline__ double2 cubic(double2 a, double2 b, double2 c, double
 // pi value of row r of one column (col = this lane's pi at row 0, rstride =
 // double2 per row); rows < 0 of the slab holding the excision end are the
 // reference's cubic ghosts.  Rare path: the orientation switch of a pi row.
-__device__ __noinline__ double2 row_or_ghost(const double2* col, int r, ptrdiff_t rstride,
+static __device__ __noinline__ double2 row_or_ghost(const double2* col, int r, ptrdiff_t rstride,
                                              int phys_lo) {
   if (r >= 0 || !phys_lo) return __ldg(col + r * rstride);
   double2 g[8];
@@ -660,20 +660,5 @@ stage_kernel(const StageArgs a) {
     atomicOr(a.flag, 1ull);
   }
 }
-
-// ---------------------------------------------------------------------------
-// Layout conversion between the reference StateVec (FieldLayout, rho fastest,
-// DD {hi, lo} pairs or plain doubles) and a device state register: 32x32
-// tiles through shared memory so both sides stay coalesced.
-// dir 0: host layout -> device (interior only); dir 1: device -> host layout
-// interior (ghosts are filled on the host).
-__global__ void relayout_kernel(const double* __restrict__ src, double* __restrict__ dst,
-                                double2* reg, int n, int nt, int nchunks, int stride, int dir);
-
-// Observer reduction (diagnostics.cpp:145-160, diagnostics.hpp:47-50,
-// diagnostics.cpp:257-283 as a precomputed linear functional): one warp.
-__global__ void observe_kernel(const double2* reg, int nchunks, int j0, const double* hw,
-                               int kobs, int jobs, int jscri, const double* pw, int nt,
-                               double* out);
 
 }  // namespace hwg

@@ -1,0 +1,18 @@
+// Launchers of the stage-kernel instantiations.  Each tier is compiled in its
+// own translation unit (hwg_stage_fast.cu, hwg_stage_dd.cu) so the build
+// parallelises; hwg_solver.cu only sees these entry points.
+#pragma once
+
+#include "hwg_dd.cuh"
+#include "hwg_kernels.cuh"
+
+namespace hwg {
+// fp64 / mixed / linear tiers (stage_kernel)
+void launch_stage_fast(const StageArgs& a, int scheme, int mode, int epi, int blocks,
+                       cudaStream_t stream);
+cudaError_t occupancy_fast(int* blocks_per_sm);
+// double-double tiers (stage_kernel_dd)
+void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks,
+                     cudaStream_t stream);
+cudaError_t occupancy_dd(int* blocks_per_sm);
+}  // namespace hwg

@@ -3,7 +3,8 @@
 // The handle mirrors EvolutionRhs (proj/src/evolve.cpp:10-38) and the time
 // loop advance_steps (evolve.cpp:237-265); the steppers' stage sequences are
 // those of ssprk33_step / ssprk104_step (proj/include/hweno/timestep.hpp:54-109)
-// with each stage one fused launch of hwg::stage_kernel.
+// with each stage one fused launch of hwg::stage_kernel (fp64 / mixed tiers)
+// or hwg::stage_kernel_dd (double-double tiers).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,18 +16,23 @@
 #include <vector>
 
 #include "../../include/hweno_gpu.h"
-#include "hwg_kernels.cuh"
+#include "hwg_launch.h"
 
 using namespace hwg;
 
 namespace {
 thread_local std::string g_create_err;
 
-struct DD {  // minimal double-double for host-side constants (precision.hpp:16-115)
+// Host double-double, an exact replica of the reference's DDReal operators
+// (proj/include/hweno/precision.hpp:16-115).  Like the reference, the host
+// side is compiled with -ffp-contract=off (build.py) so no multiply-add is
+// fused; std::fma is explicit.
+struct DD {
   double hi, lo;
 };
 inline double two_sum(double a, double b, double& e) {
-  double s = a + b, bb = s - a;
+  double s = a + b;
+  double bb = s - a;
   e = (a - (s - bb)) + (b - bb);
   return s;
 }
@@ -35,52 +41,74 @@ inline double quick_two_sum(double a, double b, double& e) {
   e = b - (s - a);
   return s;
 }
-inline DD dd_mul(DD a, DD b) {
-  double p2;
-  double p1 = a.hi * b.hi;
-  p2 = std::fma(a.hi, b.hi, -p1);
-  p2 += a.hi * b.lo + a.lo * b.hi;
-  p1 = quick_two_sum(p1, p2, p2);
-  return {p1, p2};
+inline double two_prod(double a, double b, double& e) {
+  double p = a * b;
+  e = std::fma(a, b, -p);
+  return p;
 }
-inline DD dd_sub(DD a, DD b) {
+inline DD dd_add(DD a, DD b) {
   double s2, t2;
-  double s1 = two_sum(a.hi, -b.hi, s2);
-  double t1 = two_sum(a.lo, -b.lo, t2);
+  double s1 = two_sum(a.hi, b.hi, s2);
+  double t1 = two_sum(a.lo, b.lo, t2);
   s2 += t1;
   s1 = quick_two_sum(s1, s2, s2);
   s2 += t2;
   s1 = quick_two_sum(s1, s2, s2);
   return {s1, s2};
 }
+inline DD dd_addd(DD a, double b) {
+  double s2;
+  double s1 = two_sum(a.hi, b, s2);
+  s2 += a.lo;
+  s1 = quick_two_sum(s1, s2, s2);
+  return {s1, s2};
+}
+inline DD dd_neg(DD a) { return {-a.hi, -a.lo}; }
+inline DD dd_sub(DD a, DD b) { return dd_add(a, dd_neg(b)); }
+inline DD dd_mul(DD a, DD b) {
+  double p2;
+  double p1 = two_prod(a.hi, b.hi, p2);
+  p2 += a.hi * b.lo + a.lo * b.hi;
+  p1 = quick_two_sum(p1, p2, p2);
+  return {p1, p2};
+}
+inline DD dd_muld(DD a, double b) {
+  double p2;
+  double p1 = two_prod(a.hi, b, p2);
+  p2 += a.lo * b;
+  p1 = quick_two_sum(p1, p2, p2);
+  return {p1, p2};
+}
 inline DD dd_div(DD a, DD b) {  // precision.hpp operator/
   double q1 = a.hi / b.hi;
-  DD r = dd_sub(a, dd_mul(b, {q1, 0.0}));
+  DD r = dd_sub(a, dd_muld(b, q1));
   double q2 = r.hi / b.hi;
-  r = dd_sub(r, dd_mul(b, {q2, 0.0}));
+  r = dd_sub(r, dd_muld(b, q2));
   double q3 = r.hi / b.hi;
   double s2;
   double s1 = quick_two_sum(q1, q2, s2);
-  double e;
-  double t = two_sum(s1, q3, e);
-  e += s2;
-  t = quick_two_sum(t, e, e);
-  return {t, e};
+  return dd_addd({s1, s2}, q3);
 }
-inline double ddq(double num, double den) { return dd_div({num, 0.0}, {den, 0.0}).hi; }
+inline DD I(double v) { return {v, 0.0}; }
+inline DD Q(double num, double den) { return dd_div(I(num), I(den)); }
+inline double ddq(double num, double den) { return Q(num, den).hi; }
+inline dd to_dev(DD v) { return {v.hi, v.lo}; }
 }  // namespace
 
 struct hwg_solver {
   hwg_desc d{};
+  bool ddm = false;          // double-double tier
   int n = 0, nt = 0, ntp = 0, phys_lo = 1, phys_hi = 1;
   int dev = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t own = nullptr;
-  double2* coef = nullptr;   // coefficient blocks (row, chunk) x 144 double2
-  double* cot = nullptr;     // cot(theta), padded to nchunks*32
+  int sblk = kStateBlk;      // double2 per (row, chunk) state block
+  int cblk = kCoefBlk;       // double2 per (row, chunk) coefficient block
+  double2* coef = nullptr;   // coefficient blocks
+  double* cot = nullptr;     // cot(theta) (fp64, or dd pairs), padded to nchunks*32
   double2* reg[5] = {};      // state registers, blocked layout incl. halo rows
   int nreg = 0;
-  size_t rs = 0;             // double2 per state row (nchunks * 64)
+  size_t rs = 0;             // double2 per state row (nchunks * sblk)
   size_t reg_elems = 0;      // double2 per register ((n + 2 kHalo) * rs)
   int cur = 0, scr1 = 1, scr2 = 2, scr3 = 3, scr4 = 4;
   unsigned long long* flag = nullptr;
@@ -88,6 +116,7 @@ struct hwg_solver {
   int nchunks = 0, nranges = 0, blocks = 0;
   double* stage_dev = nullptr;
   size_t stage_cap = 0;
+  DD drho{0, 0}, dtheta{0, 0}, eps{0, 0}, sigma{0, 0};
   // observers
   int kobs = -1, j0 = -1, jobs = -1;
   double* obs_w = nullptr;   // 32 horizon weights + ntheta projection weights
@@ -106,59 +135,71 @@ struct hwg_solver {
   } while (0)
 
 // ----------------------------------------------------------------------------
-// kernels declared in hwg_kernels.cuh
+// layout kernels
 namespace hwg {
 
-__global__ void relayout_kernel(const double* __restrict__ src, double* __restrict__ dst,
-                                double2* reg, int n, int nt, int nchunks, int stride, int dir) {
-  // reg points at row 0 of a blocked state register
+// host FieldLayout <-> device register (row 0 pointer), blocked; stride 2 =
+// DD {hi, lo} pairs on the host.  dd: the register holds lo limbs at +64.
+__global__ void relayout_kernel2(const double* __restrict__ src, double* __restrict__ dst,
+                                 double2* reg, int n, int nt, int nchunks, int stride, int dir,
+                                 int sblk) {
   __shared__ double tile[4][32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const size_t W = (size_t)n + 8, Hh = (size_t)nt + 4, P = W * Hh;
-  const size_t rs = (size_t)nchunks * kStateBlk;
-  if (dir == 0) {
-    for (int kk = ty; kk < 32; kk += 8) {
-      const int k = k0 + kk, j = j0 + tx;
-      if (k < nt && j < n)
-        for (int c = 0; c < 4; ++c)
-          tile[c][kk][tx] = src[(c * P + (size_t)(k + 2) * W + (j + 4)) * stride];
-    }
-    __syncthreads();
-    for (int jj = ty; jj < 32; jj += 8) {
-      const int j = j0 + jj, k = k0 + tx;
-      if (k < nt && j < n) {
-        double2* b = reg + j * rs + (size_t)(k >> 5) * kStateBlk + (k & 31);
-        b[0] = make_double2(tile[0][tx][jj], tile[1][tx][jj]);
-        b[32] = make_double2(tile[2][tx][jj], tile[3][tx][jj]);
+  const size_t rs = (size_t)nchunks * sblk;
+  const bool dd = sblk == kStateBlkDD;
+  for (int limb = 0; limb < 2; ++limb) {
+    if (limb == 1 && !dd && !(dir == 1 && stride == 2)) break;
+    const int off = limb * 64;  // lo limbs at +64 in a DD block
+    if (dir == 0) {
+      for (int kk = ty; kk < 32; kk += 8) {
+        const int k = k0 + kk, j = j0 + tx;
+        if (k < nt && j < n)
+          for (int c = 0; c < 4; ++c) {
+            const size_t o = (c * P + (size_t)(k + 2) * W + (j + 4)) * stride;
+            tile[c][kk][tx] = limb == 0 ? src[o] : (stride == 2 ? src[o + 1] : 0.0);
+          }
       }
-    }
-  } else {
-    for (int jj = ty; jj < 32; jj += 8) {
-      const int j = j0 + jj, k = k0 + tx;
-      if (k < nt && j < n) {
-        const double2* b = reg + j * rs + (size_t)(k >> 5) * kStateBlk + (k & 31);
-        double2 u = b[0], v = b[32];
-        tile[0][tx][jj] = u.x; tile[1][tx][jj] = u.y;
-        tile[2][tx][jj] = v.x; tile[3][tx][jj] = v.y;
-      }
-    }
-    __syncthreads();
-    for (int kk = ty; kk < 32; kk += 8) {
-      const int k = k0 + kk, j = j0 + tx;
-      if (k < nt && j < n)
-        for (int c = 0; c < 4; ++c) {
-          const size_t o = (c * P + (size_t)(k + 2) * W + (j + 4)) * stride;
-          dst[o] = tile[c][kk][tx];
-          if (stride == 2) dst[o + 1] = 0.0;
+      __syncthreads();
+      for (int jj = ty; jj < 32; jj += 8) {
+        const int j = j0 + jj, k = k0 + tx;
+        if (k < nt && j < n) {
+          double2* b = reg + j * rs + (size_t)(k >> 5) * sblk + (k & 31) + off;
+          b[0] = make_double2(tile[0][tx][jj], tile[1][tx][jj]);
+          b[32] = make_double2(tile[2][tx][jj], tile[3][tx][jj]);
         }
+      }
+    } else {
+      for (int jj = ty; jj < 32; jj += 8) {
+        const int j = j0 + jj, k = k0 + tx;
+        if (k < nt && j < n) {
+          double2 u = make_double2(0.0, 0.0), v = u;
+          if (limb == 0 || dd) {
+            const double2* b = reg + j * rs + (size_t)(k >> 5) * sblk + (k & 31) + off;
+            u = b[0];
+            v = b[32];
+          }
+          tile[0][tx][jj] = u.x; tile[1][tx][jj] = u.y;
+          tile[2][tx][jj] = v.x; tile[3][tx][jj] = v.y;
+        }
+      }
+      __syncthreads();
+      for (int kk = ty; kk < 32; kk += 8) {
+        const int k = k0 + kk, j = j0 + tx;
+        if (k < nt && j < n)
+          for (int c = 0; c < 4; ++c)
+            dst[(c * P + (size_t)(k + 2) * W + (j + 4)) * stride + limb] = tile[c][kk][tx];
+      }
     }
+    __syncthreads();
   }
 }
 
-// coefficient plane q (index j + ld*k, rows row0..) -> blocked coefficient member
+// coefficient plane q (index j + ld*k, rows row0..) -> blocked coefficient
+// member; lo = 1 writes the DD low limbs (block offset kCoefBlk)
 __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, double* coef,
-                            int q, int n, int nt, int nchunks) {
+                            int q, int n, int nt, int nchunks, int cblk, int lo) {
   __shared__ double tile[32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -170,7 +211,7 @@ __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, do
   for (int jj = ty; jj < 32; jj += 8) {
     const int j = j0 + jj, k = k0 + tx;
     if (j < n && k < nchunks * 32) {
-      const size_t blk = ((size_t)j * nchunks + (k >> 5)) * kCoefBlk;  // double2 units
+      const size_t blk = ((size_t)j * nchunks + (k >> 5)) * cblk + (lo ? kCoefBlk : 0);
       size_t o;
       if (q < 8) o = (blk + (q / 2) * 32 + (k & 31)) * 2 + (q % 2);
       else o = (blk + kCoefAth) * 2 + (k & 31);
@@ -179,11 +220,11 @@ __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, do
   }
 }
 
-__global__ void observe_kernel(const double2* reg, int nchunks, int j0, const double* hw,
-                               int kobs, int jobs, int jscri, const double* pw, int nt,
-                               double* out) {
-  const size_t rs = (size_t)nchunks * kStateBlk;
-  auto psi = [&](int j, int k) { return reg[j * rs + (size_t)(k >> 5) * kStateBlk + (k & 31)]; };
+__global__ void observe_kernel2(const double2* reg, int nchunks, int sblk, int j0,
+                                const double* hw, int kobs, int jobs, int jscri, const double* pw,
+                                int nt, double* out) {
+  const size_t rs = (size_t)nchunks * sblk;
+  auto psi = [&](int j, int k) { return reg[j * rs + (size_t)(k >> 5) * sblk + (k & 31)]; };
   const int lane = threadIdx.x;
   if (lane == 0) {
     // HorizonSampler::sample (diagnostics.cpp:145-160): sequential dot products
@@ -223,47 +264,25 @@ __global__ void observe_kernel(const double2* reg, int nchunks, int j0, const do
 // ----------------------------------------------------------------------------
 namespace {
 
-template <int SCH, int MODE, int EPI>
-void launch_t(const hwg_solver* s, const StageArgs& a) {
-  static bool attr = [] {
-    cudaFuncSetAttribute(stage_kernel<SCH, MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)stage_smem_bytes<EPI>());
-    return true;
-  }();
-  (void)attr;
-  stage_kernel<SCH, MODE, EPI><<<s->blocks, kWarpsPerBlock * 32, stage_smem_bytes<EPI>(),
-                                 s->stream>>>(a);
-}
-
-template <int SCH, int MODE>
-void launch_m(const hwg_solver* s, const StageArgs& a, int epi) {
-  switch (epi) {
-    case EPI_RHS: launch_t<SCH, MODE, EPI_RHS>(s, a); break;
-    case EPI_AXPY: launch_t<SCH, MODE, EPI_AXPY>(s, a); break;
-    case EPI_RK3: launch_t<SCH, MODE, EPI_RK3>(s, a); break;
-    case EPI_RK3C: launch_t<SCH, MODE, EPI_RK3C>(s, a); break;
-    case EPI_RK104_5: launch_t<SCH, MODE, EPI_RK104_5>(s, a); break;
-    default: launch_t<SCH, MODE, EPI_RK104_10>(s, a); break;
-  }
-}
-
-template <int SCH>
-void launch_s(const hwg_solver* s, const StageArgs& a, int epi) {
-  if constexpr (SCH == FD6KO) {
-    launch_m<SCH, F64>(s, a, epi);  // no weights
-  } else {
-    if (std::isinf(s->d.eps)) launch_m<SCH, LIN>(s, a, epi);
-    else if (s->d.precision == HWG_F64) launch_m<SCH, F64>(s, a, epi);
-    else launch_m<SCH, MIXED>(s, a, epi);
-  }
+int mode_of(const hwg_solver* s) {
+  if (s->d.scheme == HWG_FD6KO) return F64;  // no weights
+  if (std::isinf(s->d.eps)) return LIN;
+  const bool mixed = s->d.precision == HWG_MIXED || s->d.precision == HWG_DD_MIXED;
+  return mixed ? MIXED : F64;
 }
 
 int launch(hwg_solver* s, const StageArgs& a, int epi) {
-  switch (s->d.scheme) {
-    case HWG_WENO5: launch_s<WENO5>(s, a, epi); break;
-    case HWG_WENO3: launch_s<WENO3>(s, a, epi); break;
-    default: launch_s<FD6KO>(s, a, epi); break;
+  launch_stage_fast(a, s->d.scheme, mode_of(s), epi, s->blocks, s->stream);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    s->err = std::string("stage launch: ") + cudaGetErrorString(e);
+    return HWG_ECUDA;
   }
+  return HWG_OK;
+}
+
+int launch(hwg_solver* s, const StageArgsDD& a, int epi) {
+  launch_stage_dd(a, s->d.scheme, mode_of(s), epi, s->blocks, s->stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     s->err = std::string("stage launch: ") + cudaGetErrorString(e);
@@ -297,9 +316,44 @@ StageArgs base_args(const hwg_solver* s) {
   return a;
 }
 
-void set_io(StageArgs& a, const hwg_solver* s, int x, int out) {
-  a.x = row0(s, x);
-  a.o = row0(s, out);
+// the reference's per-call DD constants, evaluated once with its own DD ops
+StageArgsDD base_args_dd(const hwg_solver* s) {
+  StageArgsDD a{};
+  a.n = s->n; a.nt = s->nt; a.nchunks = s->nchunks;
+  a.phys_lo = s->phys_lo; a.phys_hi = s->phys_hi;
+  a.nranges = s->nranges;
+  a.negpar = s->d.parity < 0 ? 1 : 0;
+  a.eps_hi = s->eps.hi;  // demote(spec_.eps), evolve.cpp:79-80
+  a.cot = reinterpret_cast<const dd*>(s->cot);
+  a.coef = s->coef;
+  a.flag = s->flag;
+  DDConsts& K = a.k;
+  K.c1312 = to_dev(Q(13, 12));
+  K.quarter = to_dev(Q(1, 4));
+  K.d0 = to_dev(Q(1, 10)); K.d1 = to_dev(Q(6, 10)); K.d2 = to_dev(Q(3, 10));
+  K.one = to_dev(I(1));
+  K.sixth = to_dev(Q(1, 6));
+  K.third = to_dev(Q(1, 3)); K.twothird = to_dev(Q(2, 3));
+  K.half = to_dev(Q(1, 2));
+  K.inv_drho = to_dev(dd_div(I(1), s->drho));                                  // spatial.hpp:143
+  K.inv1 = to_dev(dd_div(I(1), dd_mul(I(12), s->dtheta)));                     // :211
+  K.inv2 = to_dev(dd_div(I(1), dd_mul(dd_mul(I(12), s->dtheta), s->dtheta)));  // :212
+  K.eps = to_dev(s->eps);
+  K.sigma = to_dev(s->sigma);
+  K.h60 = to_dev(dd_mul(I(60), s->drho));
+  K.h256 = to_dev(dd_mul(I(256), s->drho));
+  const double ints[16] = {4, 6, 9, 45, 8, 28, 56, 70, 16, 30, 12, 2, 3, 5, 7, 11};
+  dd* iv[16] = {&K.c4, &K.c6, &K.c9, &K.c45, &K.c8, &K.c28, &K.c56, &K.c70,
+                &K.c16, &K.c30, &K.c12, &K.c2, &K.c3, &K.c5, &K.c7, &K.c11};
+  for (int i = 0; i < 16; ++i) *iv[i] = to_dev(I(ints[i]));
+  const bool full = s->d.precision == HWG_DD_FULL;
+  // eps = inf weights in the weight scalar TW (spatial.hpp:33-38, 100-103)
+  K.lw5[0] = full ? to_dev(Q(1, 10)) : to_dev(I(1.0 / 10.0));
+  K.lw5[1] = full ? to_dev(Q(6, 10)) : to_dev(I(6.0 / 10.0));
+  K.lw5[2] = full ? to_dev(Q(3, 10)) : to_dev(I(3.0 / 10.0));
+  K.lw3[0] = full ? to_dev(Q(1, 3)) : to_dev(I(1.0 / 3.0));
+  K.lw3[1] = full ? to_dev(Q(2, 3)) : to_dev(I(2.0 / 3.0));
+  return a;
 }
 
 int ensure_regs(hwg_solver* s, int need) {
@@ -319,164 +373,170 @@ int stage_input_reg(const hwg_solver* s, int stepper, int stage) {
     return in[stage];
   }
   // rk104: U=cur, P=scr1, Q=scr2, S4=scr3, F4=scr4
-  const int P = s->scr1, Q = s->scr2, S4 = s->scr3;
-  const int in[10] = {s->cur, P, Q, P, S4, P, Q, P, Q, P};
+  const int P = s->scr1, Qr = s->scr2, S4 = s->scr3;
+  const int in[10] = {s->cur, P, Qr, P, S4, P, Qr, P, Qr, P};
   return in[stage];
 }
 
-int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, long long step) {
-  StageArgs a = base_args(s);
-  a.step = step + 1;
-  const double dt = dt_hi;
+// Stage plan shared by both tiers: registers and RK constants
+// (timestep.hpp:61-70 for ssprk33, :84-108 for ssprk104 with u^(4) kept in
+// its own register instead of a copy).  Constants in DD (the fp64 tier uses .hi).
+struct Plan {
+  int x, out, ua = -1, ub = -1, ug = -1, f = -1, epi;
+  DD ca{0, 0}, cb{0, 0}, cc{0, 0}, cg{0, 0}, cd{0, 0}, ce{0, 0};
+  int rot = 0;  // 1: swap cur<->scr1 after, 2: swap cur<->scr2 after
+};
+
+Plan make_plan(const hwg_solver* s, int stepper, int stage, DD dt) {
+  Plan p{};
   if (stepper == HWG_SSPRK33) {
-    // timestep.hpp:61-70
     if (stage == 0) {
-      set_io(a, s, s->cur, s->scr1);
-      a.cg = dt;
-      return launch(s, a, EPI_AXPY);
+      p.x = s->cur; p.out = s->scr1; p.cg = dt; p.epi = EPI_AXPY;
+    } else if (stage == 1) {
+      p.x = s->scr1; p.out = s->scr2; p.ua = s->cur; p.epi = EPI_RK3;
+      p.ca = Q(3, 4); p.cb = Q(1, 4); p.cg = dt;
+    } else {
+      p.x = s->scr2; p.out = s->scr1; p.ua = s->cur; p.epi = EPI_RK3C;
+      p.ca = Q(1, 3); p.cb = Q(2, 3); p.cg = dt; p.rot = 1;
     }
-    a.ua = row0(s, s->cur);
-    a.cg = dt;
-    if (stage == 1) {
-      set_io(a, s, s->scr1, s->scr2);
-      a.ca = 0.75; a.cb = 0.25;
-      return launch(s, a, EPI_RK3);
-    }
-    set_io(a, s, s->scr2, s->scr1);
-    a.ca = ddq(1.0, 3.0); a.cb = ddq(2.0, 3.0);
-    int rc = launch(s, a, EPI_RK3C);
-    std::swap(s->cur, s->scr1);
-    return rc;
+    return p;
   }
-  // ssprk104, timestep.hpp:84-108 (u^(4) kept in S4 instead of a copy)
-  const int U = s->cur, P = s->scr1, Q = s->scr2, S4 = s->scr3, F4 = s->scr4;
-  const DD dtd{dt_hi, dt_lo};
-  const double dt6 = dd_div(dtd, {6.0, 0.0}).hi;
-  const int ins[10] = {U, P, Q, P, S4, P, Q, P, Q, P};
-  const int outs[10] = {P, Q, P, S4, P, Q, P, Q, P, Q};
-  set_io(a, s, ins[stage], outs[stage]);
+  const int U = s->cur, P = s->scr1, Qr = s->scr2, S4 = s->scr3, F4 = s->scr4;
+  const int ins[10] = {U, P, Qr, P, S4, P, Qr, P, Qr, P};
+  const int outs[10] = {P, Qr, P, S4, P, Qr, P, Qr, P, Qr};
+  p.x = ins[stage];
+  p.out = outs[stage];
   if (stage == 4) {
-    a.ua = row0(s, U);
-    a.f = row0(s, F4);
-    a.ca = ddq(3.0, 5.0); a.cb = ddq(2.0, 5.0);
-    a.cg = dd_div(dtd, {15.0, 0.0}).hi;
-    return launch(s, a, EPI_RK104_5);
+    p.ua = U; p.f = F4; p.epi = EPI_RK104_5;
+    p.ca = Q(3, 5); p.cb = Q(2, 5); p.cg = dd_div(dt, I(15));
+  } else if (stage == 9) {
+    p.ua = U; p.ub = S4; p.ug = F4; p.epi = EPI_RK104_10;
+    p.ca = Q(1, 25); p.cb = Q(9, 25); p.cc = Q(3, 5);
+    p.cg = dt; p.cd = Q(3, 50); p.ce = Q(1, 10); p.rot = 2;
+  } else {
+    p.epi = EPI_AXPY; p.cg = dd_div(dt, I(6));
   }
-  if (stage == 9) {
-    a.ua = row0(s, U);
-    a.ub = row0(s, S4);
-    a.ug = row0(s, F4);
-    a.ca = ddq(1.0, 25.0); a.cb = ddq(9.0, 25.0); a.cc = ddq(3.0, 5.0);
-    a.cg = dt; a.cd = ddq(3.0, 50.0); a.ce = ddq(1.0, 10.0);
-    int rc = launch(s, a, EPI_RK104_10);
-    std::swap(s->cur, s->scr2);
-    return rc;
+  return p;
+}
+
+int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, long long step) {
+  const Plan p = make_plan(s, stepper, stage, DD{dt_hi, dt_lo});
+  int rc;
+  auto r0 = [&](int r) -> double2* { return r >= 0 ? row0(s, r) : nullptr; };
+  if (s->ddm) {
+    StageArgsDD a = base_args_dd(s);
+    a.step = step + 1;
+    a.x = r0(p.x); a.o = r0(p.out); a.ua = r0(p.ua); a.ub = r0(p.ub); a.ug = r0(p.ug);
+    a.f = r0(p.f);
+    a.k.ca = to_dev(p.ca); a.k.cb = to_dev(p.cb); a.k.cc = to_dev(p.cc);
+    a.k.cg = to_dev(p.cg); a.k.cd = to_dev(p.cd); a.k.ce = to_dev(p.ce);
+    rc = launch(s, a, p.epi);
+  } else {
+    StageArgs a = base_args(s);
+    a.step = step + 1;
+    a.x = r0(p.x); a.o = r0(p.out); a.ua = r0(p.ua); a.ub = r0(p.ub); a.ug = r0(p.ug);
+    a.f = r0(p.f);
+    a.ca = p.ca.hi; a.cb = p.cb.hi; a.cc = p.cc.hi; a.cg = p.cg.hi; a.cd = p.cd.hi; a.ce = p.ce.hi;
+    rc = launch(s, a, p.epi);
   }
-  a.cg = dt6;
-  return launch(s, a, EPI_AXPY);
+  if (p.rot == 1) std::swap(s->cur, s->scr1);
+  if (p.rot == 2) std::swap(s->cur, s->scr2);
+  return rc;
+}
+
+int ensure_staging(hwg_solver* s, size_t cnt) {
+  if (s->stage_cap < cnt) {
+    if (s->stage_dev) cudaFree(s->stage_dev);
+    s->stage_dev = nullptr;
+    s->stage_cap = 0;
+    CK(cudaMalloc(&s->stage_dev, cnt * sizeof(double)));
+    s->stage_cap = cnt;
+  }
+  return HWG_OK;
 }
 
 int upload_layout(hwg_solver* s, const double* host, int stride, int reg) {
   const size_t cnt = (size_t)4 * (s->n + 8) * (s->nt + 4) * stride;
-  if (s->stage_cap < cnt) {
-    if (s->stage_dev) cudaFree(s->stage_dev);
-    s->stage_dev = nullptr;
-    s->stage_cap = 0;
-    CK(cudaMalloc(&s->stage_dev, cnt * sizeof(double)));
-    s->stage_cap = cnt;
-  }
+  int rc = ensure_staging(s, cnt);
+  if (rc) return rc;
   CK(cudaMemcpyAsync(s->stage_dev, host, cnt * sizeof(double), cudaMemcpyHostToDevice, s->stream));
   dim3 grid((s->n + 31) / 32, (s->nt + 31) / 32), blk(32, 8);
-  relayout_kernel<<<grid, blk, 0, s->stream>>>(s->stage_dev, nullptr, row0(s, reg), s->n, s->nt,
-                                                s->nchunks, stride, 0);
+  relayout_kernel2<<<grid, blk, 0, s->stream>>>(s->stage_dev, nullptr, row0(s, reg), s->n, s->nt,
+                                                 s->nchunks, stride, 0, s->sblk);
   CK(cudaGetLastError());
   return HWG_OK;
 }
 
-// interior of register reg -> host FieldLayout, then the reference's ghost
-// rules on the host (evolve.cpp:40-71)
+// the reference's ghost rules (evolve.cpp:40-71) on a host FieldLayout, in
+// fp64 or (stride 2) in double-double with the reference's DD operators
+void fill_host_ghosts(const hwg_solver* s, double* u, int stride, bool dd_arith) {
+  const int n = s->n, nt = s->nt;
+  const long long W = n + 8, P = W * (nt + 4);
+  auto idx = [&](int c, int j, int k) { return (c * P + (long long)(k + 2) * W + (j + 4)) * stride; };
+  auto get = [&](int c, int j, int k) -> DD {
+    const long long o = idx(c, j, k);
+    return {u[o], stride == 2 ? u[o + 1] : 0.0};
+  };
+  auto put = [&](int c, int j, int k, DD v) {
+    const long long o = idx(c, j, k);
+    u[o] = v.hi;
+    if (stride == 2) u[o + 1] = v.lo;
+  };
+  auto cub = [&](DD a, DD b, DD c, DD d) -> DD {
+    if (dd_arith)  // WorkReal(4) * p - WorkReal(6) * q + WorkReal(4) * r - t
+      return dd_sub(dd_add(dd_sub(dd_mul(I(4), a), dd_mul(I(6), b)), dd_mul(I(4), c)), d);
+    return I(4.0 * a.hi - 6.0 * b.hi + 4.0 * c.hi - d.hi);
+  };
+  for (int k = 0; k < nt; ++k)
+    for (int c = 0; c < 4; ++c) {
+      for (int t = 1; t <= 4; ++t)
+        put(c, -t, k, cub(get(c, -t + 1, k), get(c, -t + 2, k), get(c, -t + 3, k), get(c, -t + 4, k)));
+      for (int t = 1; t <= 4; ++t)
+        put(c, n - 1 + t, k,
+            cub(get(c, n - 2 + t, k), get(c, n - 3 + t, k), get(c, n - 4 + t, k), get(c, n - 5 + t, k)));
+    }
+  const bool even = s->d.parity > 0;
+  for (int j = 0; j < n; ++j)
+    for (int c = 0; c < 4; ++c)
+      for (int t = 0; t < 2; ++t) {
+        const DD north = get(c, j, t), south = get(c, j, nt - 1 - t);
+        put(c, j, -1 - t, even ? north : dd_neg(north));
+        put(c, j, nt + t, even ? south : dd_neg(south));
+      }
+}
+
+// interior of register reg -> host FieldLayout (+ the reference's ghost rules)
 int download_layout(hwg_solver* s, double* host, int stride, int reg, bool ghosts) {
   const size_t cnt = (size_t)4 * (s->n + 8) * (s->nt + 4) * stride;
-  if (s->stage_cap < cnt) {
-    if (s->stage_dev) cudaFree(s->stage_dev);
-    s->stage_dev = nullptr;
-    s->stage_cap = 0;
-    CK(cudaMalloc(&s->stage_dev, cnt * sizeof(double)));
-    s->stage_cap = cnt;
-  }
+  int rc = ensure_staging(s, cnt);
+  if (rc) return rc;
   CK(cudaMemsetAsync(s->stage_dev, 0, cnt * sizeof(double), s->stream));
   dim3 grid((s->n + 31) / 32, (s->nt + 31) / 32), blk(32, 8);
-  relayout_kernel<<<grid, blk, 0, s->stream>>>(nullptr, s->stage_dev, row0(s, reg), s->n, s->nt,
-                                                s->nchunks, stride, 1);
+  relayout_kernel2<<<grid, blk, 0, s->stream>>>(nullptr, s->stage_dev, row0(s, reg), s->n, s->nt,
+                                                 s->nchunks, stride, 1, s->sblk);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(host, s->stage_dev, cnt * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
-  if (!ghosts) return HWG_OK;
-  const int n = s->n, nt = s->nt;
-  const long long W = n + 8, P = W * (nt + 4);
-  auto at = [&](int c, int j, int k) -> double& {
-    return host[(c * P + (long long)(k + 2) * W + (j + 4)) * stride];
-  };
-  for (int k = 0; k < nt; ++k)
-    for (int c = 0; c < 4; ++c) {
-      for (int t = 1; t <= 4; ++t)
-        at(c, -t, k) = 4.0 * at(c, -t + 1, k) - 6.0 * at(c, -t + 2, k) +
-                       4.0 * at(c, -t + 3, k) - at(c, -t + 4, k);
-      for (int t = 1; t <= 4; ++t)
-        at(c, n - 1 + t, k) = 4.0 * at(c, n - 2 + t, k) - 6.0 * at(c, n - 3 + t, k) +
-                              4.0 * at(c, n - 4 + t, k) - at(c, n - 5 + t, k);
-    }
-  const bool even = s->d.parity > 0;
-  for (int j = 0; j < n; ++j)
-    for (int c = 0; c < 4; ++c)
-      for (int t = 0; t < 2; ++t) {
-        const double north = at(c, j, t), south = at(c, j, nt - 1 - t);
-        at(c, j, -1 - t) = even ? north : -north;
-        at(c, j, nt + t) = even ? south : -south;
-      }
+  if (ghosts) fill_host_ghosts(s, host, stride, s->ddm && stride == 2);
   return HWG_OK;
-}
-
-void fill_host_ghosts(const hwg_solver* s, double* u, int stride) {
-  const int n = s->n, nt = s->nt;
-  const long long W = n + 8, P = W * (nt + 4);
-  auto at = [&](int c, int j, int k) -> double& {
-    return u[(c * P + (long long)(k + 2) * W + (j + 4)) * stride];
-  };
-  auto lo = [&](int c, int j, int k) -> double& {
-    return u[(c * P + (long long)(k + 2) * W + (j + 4)) * stride + 1];
-  };
-  for (int k = 0; k < nt; ++k)
-    for (int c = 0; c < 4; ++c) {
-      for (int t = 1; t <= 4; ++t) {
-        at(c, -t, k) = 4.0 * at(c, -t + 1, k) - 6.0 * at(c, -t + 2, k) +
-                       4.0 * at(c, -t + 3, k) - at(c, -t + 4, k);
-        if (stride == 2) lo(c, -t, k) = 0.0;
-      }
-      for (int t = 1; t <= 4; ++t) {
-        at(c, n - 1 + t, k) = 4.0 * at(c, n - 2 + t, k) - 6.0 * at(c, n - 3 + t, k) +
-                              4.0 * at(c, n - 4 + t, k) - at(c, n - 5 + t, k);
-        if (stride == 2) lo(c, n - 1 + t, k) = 0.0;
-      }
-    }
-  const bool even = s->d.parity > 0;
-  for (int j = 0; j < n; ++j)
-    for (int c = 0; c < 4; ++c)
-      for (int t = 0; t < 2; ++t) {
-        const double north = at(c, j, t), south = at(c, j, nt - 1 - t);
-        at(c, j, -1 - t) = even ? north : -north;
-        at(c, j, nt + t) = even ? south : -south;
-        if (stride == 2) { lo(c, j, -1 - t) = 0.0; lo(c, j, nt + t) = 0.0; }
-      }
 }
 
 int rhs_impl(hwg_solver* s, double* u, double* du, int stride) {
   int rc = upload_layout(s, u, stride, s->scr1);
   if (rc) return rc;
-  StageArgs a = base_args(s);
-  a.flag = nullptr;  // the RHS never freezes
-  set_io(a, s, s->scr1, s->scr2);
-  rc = launch(s, a, EPI_RHS);
+  if (s->ddm) {
+    StageArgsDD a = base_args_dd(s);
+    a.flag = nullptr;  // the RHS never freezes
+    a.x = row0(s, s->scr1);
+    a.o = row0(s, s->scr2);
+    rc = launch(s, a, EPI_RHS);
+  } else {
+    StageArgs a = base_args(s);
+    a.flag = nullptr;
+    a.x = row0(s, s->scr1);
+    a.o = row0(s, s->scr2);
+    rc = launch(s, a, EPI_RHS);
+  }
   if (rc) return rc;
   // du interior only; its ghosts stay as the caller gave them
   const int n = s->n, nt = s->nt;
@@ -490,24 +550,16 @@ int rhs_impl(hwg_solver* s, double* u, double* du, int stride) {
       const size_t o = (c * P + (long long)(k + 2) * W + 4) * stride;
       std::memcpy(du + o, tmp.data() + o, sizeof(double) * n * stride);
     }
-  fill_host_ghosts(s, u, stride);
+  fill_host_ghosts(s, u, stride, s->ddm && stride == 2);
   return HWG_OK;
 }
 
 DD tau_of(long long step, double dt_hi, double dt_lo) {  // WorkReal(double(s)) * dt
-  return dd_mul({(double)step, 0.0}, {dt_hi, dt_lo});
+  return dd_mul(I((double)step), {dt_hi, dt_lo});
 }
 
-}  // namespace
-
-// ----------------------------------------------------------------------------
-extern "C" {
-
-const char* hwg_last_error(const hwg_solver* s) {
-  return s ? s->err.c_str() : g_create_err.c_str();
-}
-
-int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_solver** out) {
+int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, const double* cotth,
+                const double* cot_lo, bool ddm, hwg_solver** out) {
   *out = nullptr;
   if (!d || !coef || !cotth) {
     g_create_err = "hwg_create: null argument";
@@ -519,36 +571,44 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
     g_create_err = "EvolutionRhs: grid below stencil support";
     return HWG_EINVAL;
   }
-  if (d->scheme < 0 || d->scheme > 2 || d->precision < 0 || d->precision > 1 ||
-      !(d->drho > 0.0) || !(d->dtheta > 0.0)) {
+  const bool prec_ok = ddm ? (d->precision == HWG_DD_FULL || d->precision == HWG_DD_MIXED)
+                           : (d->precision == HWG_F64 || d->precision == HWG_MIXED);
+  if (d->scheme < 0 || d->scheme > 2 || !prec_ok || !(d->drho > 0.0) || !(d->dtheta > 0.0)) {
     g_create_err = "hwg_create: invalid scheme/precision/spacing";
     return HWG_EINVAL;
   }
   const int ld = d->coef_ld > 0 ? d->coef_ld : nglob;
-  const int row0 = d->coef_row0 >= 0 ? d->coef_row0 : d->rho_offset;
+  const int row0_ = d->coef_row0 >= 0 ? d->coef_row0 : d->rho_offset;
   // lam sign structure (evolve.cpp:19-30): lam < 0 on [0, split), >= 0 after
   const double* lam = coef + (size_t)ld * d->ntheta;
   for (int k = 0; k < d->ntheta; ++k) {
     int j = 0;
-    while (j < d->nrho && lam[(size_t)(row0 + j) + (size_t)ld * k] < 0.0) ++j;
+    while (j < d->nrho && lam[(size_t)(row0_ + j) + (size_t)ld * k] < 0.0) ++j;
     for (; j < d->nrho; ++j)
-      if (lam[(size_t)(row0 + j) + (size_t)ld * k] < 0.0) {
+      if (lam[(size_t)(row0_ + j) + (size_t)ld * k] < 0.0) {
         g_create_err = "EvolutionRhs: lam changes sign more than once along a row";
         return HWG_ERUNTIME;
       }
   }
   auto* s = new hwg_solver();
   s->d = *d;
+  s->ddm = ddm;
   s->d.nrho_global = nglob;
   s->n = d->nrho;
   s->nt = d->ntheta;
   s->ntp = (d->ntheta + 31) / 32 * 32;
   s->nchunks = s->ntp / 32;
-  s->rs = (size_t)s->nchunks * kStateBlk;
+  s->sblk = ddm ? kStateBlkDD : kStateBlk;
+  s->cblk = ddm ? kCoefBlkDD : kCoefBlk;
+  s->rs = (size_t)s->nchunks * s->sblk;
   s->phys_lo = d->rho_offset == 0;
   s->phys_hi = d->rho_offset + d->nrho == nglob;
   s->dev = d->device;
   s->reg_elems = (size_t)(s->n + 2 * kHalo) * s->rs;
+  s->drho = {d->drho, ddm ? d->drho_lo : 0.0};
+  s->dtheta = {d->dtheta, ddm ? d->dtheta_lo : 0.0};
+  s->eps = {d->eps, ddm ? d->eps_lo : 0.0};
+  s->sigma = {d->sigma, ddm ? d->sigma_lo : 0.0};
   auto fail = [&](int rc) {
     g_create_err = s->err;
     hwg_destroy(s);
@@ -569,10 +629,10 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
   } while (0)
   CK(cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking));
   s->stream = s->own;
-  const size_t CB = (size_t)s->n * s->nchunks * kCoefBlk;
+  const size_t CB = (size_t)s->n * s->nchunks * s->cblk;
   CK(cudaMalloc(&s->coef, CB * sizeof(double2)));
   CK(cudaMemsetAsync(s->coef, 0, CB * sizeof(double2), s->stream));
-  CK(cudaMalloc(&s->cot, s->ntp * sizeof(double)));
+  CK(cudaMalloc(&s->cot, 2 * s->ntp * sizeof(double)));
   CK(cudaMalloc(&s->flag, 2 * sizeof(unsigned long long)));
   CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
   CK(cudaMallocHost(&s->hflag, 2 * sizeof(unsigned long long)));
@@ -581,24 +641,38 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
   CK(cudaMalloc(&s->obs_w, (32 + s->ntp) * sizeof(double)));
   CK(cudaMemsetAsync(s->obs_w, 0, (32 + s->ntp) * sizeof(double), s->stream));
   // coefficients: upload each reference plane (rows of this handle) and
-  // transpose on the device into (row, theta) order
+  // transpose on the device into the blocked layout
   {
     double* tmp = nullptr;
     const size_t plane_src = (size_t)ld * s->nt;
     CK(cudaMalloc(&tmp, plane_src * sizeof(double)));
     dim3 grid((s->n + 31) / 32, s->nchunks), blk(32, 8);
-    for (int q = 0; q < 9; ++q) {
-      CK(cudaMemcpyAsync(tmp, coef + q * plane_src, plane_src * sizeof(double),
-                         cudaMemcpyHostToDevice, s->stream));
-      coef_kernel<<<grid, blk, 0, s->stream>>>(tmp, ld, row0, reinterpret_cast<double*>(s->coef), q,
-                                                s->n, s->nt, s->nchunks);
-      CK(cudaGetLastError());
+    for (int limb = 0; limb < (ddm ? 2 : 1); ++limb) {
+      const double* src = limb ? coef_lo : coef;
+      for (int q = 0; q < 9; ++q) {
+        if (src) {
+          CK(cudaMemcpyAsync(tmp, src + q * plane_src, plane_src * sizeof(double),
+                             cudaMemcpyHostToDevice, s->stream));
+        } else {
+          CK(cudaMemsetAsync(tmp, 0, plane_src * sizeof(double), s->stream));
+        }
+        coef_kernel<<<grid, blk, 0, s->stream>>>(tmp, ld, row0_, reinterpret_cast<double*>(s->coef),
+                                                  q, s->n, s->nt, s->nchunks, s->cblk, limb);
+        CK(cudaGetLastError());
+      }
     }
     CK(cudaStreamSynchronize(s->stream));
     cudaFree(tmp);
-    std::vector<double> c(s->ntp, 0.0);
-    for (int k = 0; k < s->nt; ++k) c[k] = cotth[k];
-    CK(cudaMemcpy(s->cot, c.data(), s->ntp * sizeof(double), cudaMemcpyHostToDevice));
+    std::vector<double> c(2 * s->ntp, 0.0);
+    for (int k = 0; k < s->nt; ++k) {
+      if (ddm) {
+        c[2 * k] = cotth[k];
+        c[2 * k + 1] = cot_lo ? cot_lo[k] : 0.0;
+      } else {
+        c[k] = cotth[k];
+      }
+    }
+    CK(cudaMemcpy(s->cot, c.data(), 2 * s->ntp * sizeof(double), cudaMemcpyHostToDevice));
   }
   {
     int rc = ensure_regs(s, 3);
@@ -608,14 +682,7 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
   {
     int nsm = 148, occ = 1;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->dev));
-    cudaFuncAttributes fa;
-    CK(cudaFuncGetAttributes(&fa, stage_kernel<WENO5, F64, EPI_RK3>));
-    CK(cudaFuncSetAttribute(stage_kernel<WENO5, F64, EPI_RK3>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)stage_smem_bytes<EPI_RK3>()));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stage_kernel<WENO5, F64, EPI_RK3>,
-                                                     kWarpsPerBlock * 32,
-                                                     stage_smem_bytes<EPI_RK3>()));
+    CK(ddm ? occupancy_dd(&occ) : occupancy_fast(&occ));
     const long long target = (long long)nsm * std::max(occ, 1) * kWarpsPerBlock;
     long long nr = std::max<long long>(1, target / s->nchunks);
     nr = std::min<long long>(nr, std::max(1, s->n / 8));  // >= 8 rows per range
@@ -634,6 +701,24 @@ int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_s
   } while (0)
   *out = s;
   return HWG_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+extern "C" {
+
+const char* hwg_last_error(const hwg_solver* s) {
+  return s ? s->err.c_str() : g_create_err.c_str();
+}
+
+int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_solver** out) {
+  return create_impl(d, coef, nullptr, cotth, nullptr, false, out);
+}
+
+int hwg_create_dd(const hwg_desc* d, const double* coef_hi, const double* coef_lo,
+                  const double* cot_hi, const double* cot_lo, hwg_solver** out) {
+  return create_impl(d, coef_hi, coef_lo, cot_hi, cot_lo, true, out);
 }
 
 void hwg_destroy(hwg_solver* s) {
@@ -773,9 +858,9 @@ int hwg_set_observers(hwg_solver* s, int kobs, int j0, const double* hw, int job
 }
 
 int hwg_observe(hwg_solver* s, hwg_observables* out) {
-  observe_kernel<<<1, 32, 0, s->stream>>>(row0(s, s->cur), s->nchunks, s->j0, s->obs_w, s->kobs,
-                                           s->jobs, s->phys_hi ? s->n - 1 : -1, s->obs_w + 32,
-                                           s->nt, s->obs_dev);
+  observe_kernel2<<<1, 32, 0, s->stream>>>(row0(s, s->cur), s->nchunks, s->sblk, s->j0, s->obs_w,
+                                            s->kobs, s->jobs, s->phys_hi ? s->n - 1 : -1,
+                                            s->obs_w + 32, s->nt, s->obs_dev);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(s->obs_host, s->obs_dev, 14 * sizeof(double), cudaMemcpyDeviceToHost,
                      s->stream));

@@ -30,7 +30,7 @@ _dp = C.POINTER(C.c_double)
 _vp = C.c_void_p
 
 SCHEMES = {"weno5": 0, "weno3": 1, "fd6ko": 2}
-PRECISIONS = {"f64": 0, "mixed": 1}
+PRECISIONS = {"f64": 0, "mixed": 1, "dd-full": 2, "dd-mixed": 3}
 STEPPERS = {"ssprk33": 0, "ssprk104": 1}
 STAGES = {"ssprk33": 3, "ssprk104": 10}
 HALO = 4
@@ -41,7 +41,8 @@ class HwgDesc(C.Structure):
                 ("dtheta", C.c_double), ("parity", C.c_int), ("scheme", C.c_int),
                 ("precision", C.c_int), ("eps", C.c_double), ("sigma", C.c_double),
                 ("device", C.c_int), ("rho_offset", C.c_int), ("nrho_global", C.c_int),
-                ("coef_ld", C.c_int), ("coef_row0", C.c_int)]
+                ("coef_ld", C.c_int), ("coef_row0", C.c_int), ("drho_lo", C.c_double),
+                ("dtheta_lo", C.c_double), ("eps_lo", C.c_double), ("sigma_lo", C.c_double)]
 
 
 class HwgRunStats(C.Structure):
@@ -64,6 +65,7 @@ HOOK = C.CFUNCTYPE(None, C.c_longlong, C.c_double, C.c_double, C.POINTER(HwgObse
 _lib.hwg_last_error.restype = C.c_char_p
 _lib.hwg_last_error.argtypes = [_vp]
 _lib.hwg_create.argtypes = [C.POINTER(HwgDesc), _dp, _dp, C.POINTER(_vp)]
+_lib.hwg_create_dd.argtypes = [C.POINTER(HwgDesc), _dp, _dp, _dp, _dp, C.POINTER(_vp)]
 _lib.hwg_destroy.argtypes = [_vp]
 _lib.hwg_set_stream.argtypes = [_vp, _vp, C.c_int]
 for _f in ("hwg_set_state_dd", "hwg_get_state_dd", "hwg_set_state", "hwg_get_state"):
@@ -83,7 +85,7 @@ _lib.hwg_status.argtypes = [_vp, C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.
 _lib.hwg_launch_info.argtypes = [_vp] + [C.POINTER(C.c_int)] * 5
 _lib.hwg_synchronize.argtypes = [_vp]
 
-EXPORTED = ["hwg_create", "hwg_destroy", "hwg_last_error", "hwg_set_stream", "hwg_set_state_dd",
+EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg_set_stream", "hwg_set_state_dd",
             "hwg_get_state_dd", "hwg_set_state", "hwg_get_state", "hwg_rhs", "hwg_rhs_dd",
             "hwg_advance", "hwg_set_observers", "hwg_observe", "hwg_launch_stage",
             "hwg_launch_steps", "hwg_stage_input", "hwg_register_ptr",
@@ -101,8 +103,10 @@ def _p(a: np.ndarray):
 
 @dataclass
 class SchemeSpec:
-    """SchemeSpec (proj/include/hweno/evolve.hpp:37-42); mode is the GPU tier
-    ('f64' ~ reference full, 'mixed' ~ reference mixed)."""
+    """SchemeSpec (proj/include/hweno/evolve.hpp:37-42); mode is the GPU tier:
+    'f64' (fp64 state + weights, ~ reference full), 'mixed' (fp64 state, fp32
+    weights, ~ reference mixed) — one tier below the reference —
+    or 'dd-full' / 'dd-mixed', the reference's own double-double precisions."""
     scheme: str = "weno5"
     mode: str = "mixed"
     eps: float = 1e-6
@@ -123,14 +127,25 @@ class GpuEvolution:
     def __init__(self, nrho: int, ntheta: int, drho: float, dtheta: float, parity: int,
                  coef: np.ndarray, cotth: np.ndarray, spec: SchemeSpec = SchemeSpec(),
                  device: int = 0, rho_offset: int = 0, nrho_global: int | None = None,
-                 coef_ld: int = 0, coef_row0: int = -1):
+                 coef_ld: int = 0, coef_row0: int = -1, coef_lo: np.ndarray | None = None,
+                 cot_lo: np.ndarray | None = None, drho_lo: float = 0.0, dtheta_lo: float = 0.0,
+                 eps_lo: float = 0.0, sigma_lo: float = 0.0):
         self._coef = np.ascontiguousarray(coef, dtype=np.float64).ravel()
         self._cot = np.ascontiguousarray(cotth, dtype=np.float64)
         d = HwgDesc(nrho, ntheta, drho, dtheta, parity, SCHEMES[spec.scheme],
                     PRECISIONS[spec.mode], spec.eps, spec.sigma, device, rho_offset,
-                    nrho_global or nrho, coef_ld, coef_row0)
+                    nrho_global or nrho, coef_ld, coef_row0, drho_lo, dtheta_lo, eps_lo, sigma_lo)
         h = _vp()
-        rc = _lib.hwg_create(C.byref(d), _p(self._coef), _p(self._cot), C.byref(h))
+        self.dd = spec.mode.startswith("dd")
+        if self.dd:
+            lo = np.zeros_like(self._coef) if coef_lo is None else np.ascontiguousarray(
+                coef_lo, dtype=np.float64).ravel()
+            clo = np.zeros_like(self._cot) if cot_lo is None else np.ascontiguousarray(
+                cot_lo, dtype=np.float64)
+            rc = _lib.hwg_create_dd(C.byref(d), _p(self._coef), _p(lo), _p(self._cot), _p(clo),
+                                    C.byref(h))
+        else:
+            rc = _lib.hwg_create(C.byref(d), _p(self._coef), _p(self._cot), C.byref(h))
         if rc != 0:
             msg = _lib.hwg_last_error(None).decode()
             if rc == 2:
@@ -143,11 +158,16 @@ class GpuEvolution:
 
     @classmethod
     def from_reference(cls, ref, spec: SchemeSpec | None = None, device: int = 0):
-        """From a reference handle (oracle.RefSolver) — used by tests only."""
+        """From a reference handle (oracle.RefSolver) — used by tests only.
+        The DD tiers take the reference's low limbs too."""
         spec = spec or SchemeSpec(ref.scheme, "f64" if ref.mode == "full" else "mixed",
                                   ref.eps, ref.sigma)
+        kw = {}
+        if spec.mode.startswith("dd"):
+            kw = dict(coef_lo=ref.coef_lo, cot_lo=ref.cotth_lo, drho_lo=ref.drho_lo,
+                      dtheta_lo=ref.dtheta_lo)
         return cls(ref.nrho, ref.ntheta, ref.drho, ref.dtheta, ref.parity, ref.coef, ref.cotth,
-                   spec, device)
+                   spec, device, **kw)
 
     def close(self):
         if getattr(self, "h", None):
@@ -199,6 +219,17 @@ class GpuEvolution:
         du = np.zeros(self.shape) if du is None else np.ascontiguousarray(du).copy()
         self._chk(_lib.hwg_rhs(self.h, _p(u), _p(du)))
         return u, du
+
+    def rhs_dd(self, hi: np.ndarray, lo: np.ndarray):
+        """EvolutionRhs::operator() on a DDReal StateVec: ((u_hi, u_lo), (du_hi, du_lo))."""
+        dd = np.empty(hi.size * 2)
+        dd[0::2] = hi.ravel()
+        dd[1::2] = lo.ravel()
+        du = np.zeros_like(dd)
+        self._chk(_lib.hwg_rhs_dd(self.h, _p(dd), _p(du)))
+        sh = self.shape
+        return ((dd[0::2].reshape(sh).copy(), dd[1::2].reshape(sh).copy()),
+                (du[0::2].reshape(sh).copy(), du[1::2].reshape(sh).copy()))
 
     # ------------------------------------------------------------------ loop
     def advance(self, stepper: str, dt, step_begin: int, step_end: int, every: int = 1,

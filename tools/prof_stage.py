@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--ntheta", type=int, default=512)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--stepper", default="ssprk33")
     a = ap.parse_args()
     import torch
     from paper_2010_04760_b200 import hwgpu, synthetic
@@ -30,16 +31,19 @@ def main():
     g = hwgpu.GpuEvolution(a.nrho, a.ntheta, prob["drho"], prob["dtheta"], prob["parity"],
                            prob["coef"], prob["cotth"], hwgpu.SchemeSpec(a.scheme, a.mode))
     g.set_state(synthetic.initial_state(prob))
-    dt = synthetic.select_dt(prob)
-    g.launch_steps("ssprk33", dt, 0, a.warmup)
+    dt = synthetic.select_dt(prob, a.stepper)
+    ns = 3 if a.stepper == "ssprk33" else 10
+    g.launch_steps(a.stepper, dt, 0, a.warmup)
     g.synchronize()
     t0 = time.perf_counter()
-    g.launch_steps("ssprk33", dt, a.warmup, a.steps)
+    g.launch_steps(a.stepper, dt, a.warmup, a.steps)
     g.synchronize()
     wall = time.perf_counter() - t0
     P = a.nrho * a.ntheta
-    print(f"{a.mode} {a.scheme} {a.nrho}x{a.ntheta}: {a.steps} steps {wall * 1e3:.3f} ms, "
-          f"{P * 3 * a.steps / wall:.3e} upd/s, launch {g.launch_info()}, "
+    bps = 157.33 if ns == 3 else 152.0
+    rate = P * ns * a.steps / wall
+    print(f"{a.mode} {a.scheme} {a.stepper} {a.nrho}x{a.ntheta}: {a.steps} steps {wall * 1e3:.3f} ms, "
+          f"{rate:.3e} upd/s, {rate * bps / 1e9:.0f} GB/s algorithmic, launch {g.launch_info()}, "
           f"blew_up={g.status()}")
 
 
