@@ -191,9 +191,11 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- B200 arm
-def time_mode(args, mode, prob, world, rank, dev, torch, dist):
+def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmup=None):
     from paper_2010_04760_b200 import hwgpu, slabs, synthetic
     spec = hwgpu.SchemeSpec("weno5", mode)
+    K = steps or args.steps
+    W = args.warmup if warmup is None else warmup
     g = hwgpu.GpuEvolution(prob["nrho"], prob["ntheta"], prob["drho"], prob["dtheta"],
                            prob["parity"], prob["coef"], prob["cotth"], spec, device=dev,
                            rho_offset=prob["rho_offset"], nrho_global=prob["nrho_global"],
@@ -205,13 +207,12 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist):
     dt = synthetic.select_dt(prob, "ssprk33")
     runner = slabs.DistSlab(g, rank, world, "weno5")
     P = prob["nrho"] * prob["ntheta"]
-    for q in range(args.warmup):
+    for q in range(W):
         runner.step("ssprk33", dt, q)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    K = args.steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(3 * K)]
     t_start = torch.cuda.Event(enable_timing=True)
@@ -222,7 +223,7 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist):
         for st in range(3):
             runner.exchange(g.stage_input("ssprk33", st))
             evs[i][0].record(stream)
-            g.launch_stage("ssprk33", st, dt, args.warmup + q)
+            g.launch_stage("ssprk33", st, dt, W + q)
             evs[i][1].record(stream)
             i += 1
     t_end.record(stream)
@@ -238,11 +239,12 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist):
         raise RuntimeError(f"benchmark state blew up ({mode})")
     value = world * P * 3 * K / (total_ms / 1000.0)
     # algorithmic bytes per launch: stage 1 136 B/pt, 2-3 168 B/pt
-    bytes_per_step = P * (136 + 168 + 168)
+    # (fp64 state 32 B + coefficients 72 B); double-double tiers twice that
+    bytes_per_step = P * (136 + 168 + 168) * (2 if mode.startswith("dd") else 1)
     kern_ms = float(stage_ms.sum())
     achieved = bytes_per_step * K / (kern_ms / 1000.0) / 1e9
     return g, dict(value=value, total_ms=total_ms, stage_ms=stage_ms, achieved_gbs=achieved,
-                   kern_ms=kern_ms, P=P, dt=dt, u0=u0)
+                   kern_ms=kern_ms, P=P, dt=dt, K=K)
 
 
 def e2e_mode(g, args, prob, world, rank, torch, dist, dt):
@@ -305,6 +307,17 @@ def run_b200(args):
     clocks.stop()
     head = results[args.mode]
     g = handles[args.mode]
+    for m in list(handles):
+        if m != args.mode:
+            handles.pop(m).close()
+    # the reference's own precisions (double-double tiers, bitwise equal to the
+    # reference library): the paper's mixed-vs-full experiment on B200
+    if not args.no_dd:
+        for mode in ("dd-mixed", "dd-full"):
+            gd, r = time_mode(args, mode, prob, world, rank, dev, torch, dist,
+                              steps=max(1, min(3, args.steps)), warmup=1)
+            gd.close()
+            results[mode] = r
     e2e = e2e_mode(g, args, prob, world, rank, torch, dist, head["dt"])
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -349,12 +362,15 @@ def run_b200(args):
                 "path": "C ABI hwg_set_state + 1 RK3 step + hwg_get_state (host FieldLayout fp64)"},
         "gpu_launches": 3 * K,
         "launch": info,
-        "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / K,
+        "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / r["K"], "steps": r["K"],
                       "stage_kernel_gbs": r["achieved_gbs"], "frac": r["achieved_gbs"] / peak,
                       "stage_ms_mean": [float(x) for x in r["stage_ms"].mean(axis=0)]}
                   for m, r in results.items()},
         "mixed_vs_fp64_speedup": results["mixed"]["value"] / results["f64"]["value"],
     }
+    if "dd-full" in results:
+        line["dd_mixed_vs_dd_full_speedup"] = (results["dd-mixed"]["value"] /
+                                               results["dd-full"]["value"])
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
@@ -375,6 +391,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dd", action="store_true")
     ap.add_argument("--ref-nrho", type=int, default=1024)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -15,10 +15,14 @@
 // Semantics follow proj/src/evolve.cpp:10-265: operator() fills u's ghosts and
 // writes du's interior; advance_steps fires the hook at s % every == 0, at the
 // first and at the last step (with tau = s * dt in double-double), stops at
-// the first inadmissible state and reports RunStats.  The GPU tiers are one
-// below the reference's: SchemeSpec::mode full -> HWG_F64,
-// mixed -> HWG_MIXED (fp32 weights).  Errors surface as the reference's
-// exception types.
+// the first inadmissible state and reports RunStats.  Errors surface as the
+// reference's exception types.
+//
+// Precision: Tier::exact (default) runs the double-double GPU tiers, which
+// reproduce the reference's full / mixed modes BIT FOR BIT (SchemeSpec::mode
+// full -> HWG_DD_FULL, mixed -> HWG_DD_MIXED).  Tier::fast runs one tier
+// below: full -> HWG_F64, mixed -> HWG_MIXED (fp32 weights),
+// ~10-20x faster and within 1e-12 / 1e-6 of the reference.
 #pragma once
 
 #include <chrono>
@@ -40,20 +44,28 @@ inline void check(int rc, const hwg_solver* s) {
   throw std::runtime_error(msg);
 }
 
+enum class Tier { exact, fast };
+
 class GpuEvolutionRhs {
  public:
   GpuEvolutionRhs(const hweno::Grid& g, const hweno::CoefficientSet& cs,
                   const hweno::PhysicalParams& p, const hweno::SchemeSpec& spec,
-                  int device = 0)
+                  int device = 0, Tier tier = Tier::exact)
       : lay_{g.nrho, g.ntheta}, spec_(spec) {
     const size_t P = size_t(g.nrho) * g.ntheta;
     const std::vector<hweno::WorkReal>* src[9] = {&cs.b,     &cs.lam,   &cs.w_re,
                                                   &cs.w_im,  &cs.bt_re, &cs.bt_im,
                                                   &cs.c_re,  &cs.c_im,  &cs.ath};
-    std::vector<double> planes(9 * P), cot(g.ntheta);
+    std::vector<double> planes(9 * P), planes_lo(9 * P), cot(g.ntheta), cot_lo(g.ntheta);
     for (int q = 0; q < 9; ++q)
-      for (size_t i = 0; i < P; ++i) planes[q * P + i] = (*src[q])[i].hi;
-    for (int k = 0; k < g.ntheta; ++k) cot[k] = cs.cotth[k].hi;
+      for (size_t i = 0; i < P; ++i) {
+        planes[q * P + i] = (*src[q])[i].hi;
+        planes_lo[q * P + i] = (*src[q])[i].lo;
+      }
+    for (int k = 0; k < g.ntheta; ++k) {
+      cot[k] = cs.cotth[k].hi;
+      cot_lo[k] = cs.cotth[k].lo;
+    }
     hwg_desc d{};
     d.nrho = g.nrho;
     d.ntheta = g.ntheta;
@@ -63,15 +75,25 @@ class GpuEvolutionRhs {
     d.scheme = spec.scheme == hweno::Scheme::weno5   ? HWG_WENO5
                : spec.scheme == hweno::Scheme::weno3 ? HWG_WENO3
                                                      : HWG_FD6KO;
-    d.precision = spec.mode == hweno::PrecisionMode::full ? HWG_F64 : HWG_MIXED;
+    const bool full = spec.mode == hweno::PrecisionMode::full;
+    if (tier == Tier::exact) d.precision = full ? HWG_DD_FULL : HWG_DD_MIXED;
+    else d.precision = full ? HWG_F64 : HWG_MIXED;
     d.eps = spec.eps.hi;
     d.sigma = spec.sigma.hi;
+    d.drho_lo = g.drho.lo;
+    d.dtheta_lo = g.dtheta.lo;
+    d.eps_lo = spec.eps.lo;
+    d.sigma_lo = spec.sigma.lo;
     d.device = device;
     d.rho_offset = 0;
     d.nrho_global = g.nrho;
     d.coef_ld = g.nrho;
     d.coef_row0 = 0;
-    check(hwg_create(&d, planes.data(), cot.data(), &h_), nullptr);
+    if (tier == Tier::exact)
+      check(hwg_create_dd(&d, planes.data(), planes_lo.data(), cot.data(), cot_lo.data(), &h_),
+            nullptr);
+    else
+      check(hwg_create(&d, planes.data(), cot.data(), &h_), nullptr);
   }
   ~GpuEvolutionRhs() { hwg_destroy(h_); }
   GpuEvolutionRhs(const GpuEvolutionRhs&) = delete;
