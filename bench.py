@@ -248,31 +248,44 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
 
 
 def e2e_mode(g, args, prob, world, rank, torch, dist, dt):
-    """Same metric through the C ABI with HOST buffers: per step
-    hwg_set_state (host FieldLayout -> device) + one RK3 step + hwg_get_state."""
+    """Same metric through the C ABI with HOST buffers (pinned, as the
+    contract allows): per step hwg_set_state (host FieldLayout -> device) +
+    one RK3 step + hwg_get_state (device -> host FieldLayout, ghosts filled)."""
     from paper_2010_04760_b200 import synthetic
-    u = synthetic.initial_state(prob)
-    out = np.zeros_like(u)
+    from paper_2010_04760_b200.hwgpu import _lib, _p
+    u0 = synthetic.initial_state(prob)
+    u = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
+    u[...] = u0
+    out = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
     ke = max(1, min(args.e2e_steps, args.steps))
     g.set_state(u)
     g.launch_steps("ssprk33", dt, 0, 1)
-    g.get_state()  # warm the staging buffers
+    g._chk(_lib.hwg_get_state(g.h, _p(out)))  # warm the staging buffers
     if world > 1:
         dist.barrier()
+    t_set = t_step = t_get = 0.0
     t0 = time.perf_counter()
     for q in range(ke):
+        a = time.perf_counter()
         g.set_state(u)
+        b = time.perf_counter()
         g.launch_steps("ssprk33", dt, q, 1)
-        from paper_2010_04760_b200.hwgpu import _lib, _p
+        g.synchronize()
+        c = time.perf_counter()
         g._chk(_lib.hwg_get_state(g.h, _p(out)))
+        d = time.perf_counter()
+        t_set += b - a
+        t_step += c - b
+        t_get += d - c
     wall = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([wall], device=f"cuda:{torch.cuda.current_device()}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wall = float(t.item())
     P = prob["nrho"] * prob["ntheta"]
-    return dict(value=world * P * 3 * ke / wall, steps=ke,
-                h2d=int(u.nbytes), d2h=int(out.nbytes))
+    return dict(value=world * P * 3 * ke / wall, steps=ke, h2d=int(u.nbytes), d2h=int(out.nbytes),
+                ms=dict(set_state=1e3 * t_set / ke, step=1e3 * t_step / ke,
+                        get_state=1e3 * t_get / ke))
 
 
 def run_b200(args):
@@ -358,8 +371,9 @@ def run_b200(args):
                      "bytes_per_point_stage": 157.33},
         "clocks": clocks.summary(),
         "e2e": {"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
-                "d2h_bytes_per_step": e2e["d2h"], "steps": e2e["steps"],
-                "path": "C ABI hwg_set_state + 1 RK3 step + hwg_get_state (host FieldLayout fp64)"},
+                "d2h_bytes_per_step": e2e["d2h"], "steps": e2e["steps"], "ms_per_step": e2e["ms"],
+                "path": "C ABI hwg_set_state + 1 RK3 step + hwg_get_state (pinned host "
+                        "FieldLayout fp64)"},
         "gpu_launches": 3 * K,
         "launch": info,
         "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / r["K"], "steps": r["K"],

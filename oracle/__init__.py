@@ -69,6 +69,9 @@ def ref_lib():
         lib.ref_select_dt.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp]
         lib.ref_advance.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, C.c_long, C.c_long,
                                     _dp, C.c_long, C.c_int, _dp, C.c_long, _lp, _dp]
+        lib.ref_run_series.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double,
+                                       C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                       _dp, C.c_long, _lp, _dp]
         lib.ref_horizon_weights.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int), _dp]
         lib.ref_projection_weights.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp]
         lib.ref_multipole_project.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
@@ -226,6 +229,21 @@ class RefSolver:
         st = dict(steps_done=stats[0], blew_up=bool(stats[1]), blowup_step=stats[2],
                   n_obs=stats[3], wall_seconds=wall.value)
         return u, st, obs[: 9 * stats[3]].reshape(-1, 9)
+
+    def run_series(self, init: Physics, stepper="ssprk104", cfl=0.5, tau_end=500.0,
+                   cadence=0.25, observer_rho=10.0, max_rows=200000):
+        """execute_run's time loop + observer hook (driver.cpp:22-93): returns
+        (rows (n, 15): tau, phi, dphi1..3, obs, proj, scri as re/im, stats)."""
+        out = np.zeros(15 * max_rows)
+        stats = (C.c_long * 5)()
+        wall = C.c_double()
+        _chk(ref_lib().ref_run_series(self.h, init.ell, init.center, init.width, init.amplitude,
+                                      STEPPERS[stepper], cfl, tau_end, cadence, observer_rho,
+                                      _ptr(out), max_rows, stats, C.byref(wall)))
+        n = stats[3]
+        return out[:15 * n].reshape(n, 15), dict(steps_done=stats[0], blew_up=bool(stats[1]),
+                                                  blowup_step=stats[2], planned=stats[4],
+                                                  wall_seconds=wall.value)
 
     def horizon_weights(self, ktheta):
         j0 = C.c_int()

@@ -11,8 +11,12 @@
 #include <cstring>
 #include <vector>
 
+#include <chrono>
+#include <filesystem>
+
 #include "hweno/diagnostics.hpp"
 #include "hweno/evolve.hpp"
+#include "hweno/io.hpp"
 #include "hweno_gpu_dropin.hpp"
 
 using namespace hweno;
@@ -120,6 +124,69 @@ int main(int argc, char** argv) {
     const bool ok2 = rn / rd <= (exact ? 0.0 : (mode == 0 ? 1e-13 : 1e-6)) && gh <= 1e-13;
     std::printf("  rhs rel %.3e ghost diff %.3e %s\n", rn / rd, gh, ok2 ? "OK" : "FAIL");
     bad += !ok2;
+  }
+  // ---- §8f-2: threaded coefficient assembly, bitwise vs the serial reference
+  {
+    PhysicalParams p;
+    p.M = WorkReal(1);
+    p.a = WorkReal(1);
+    p.spin = -2;
+    p.mmode = 2;
+    p.S = WorkReal(20);
+    Grid g = make_grid(2048, 64, p);
+    auto t0 = std::chrono::steady_clock::now();
+    CoefficientSet a = assemble_coefficients(g, p);
+    auto t1 = std::chrono::steady_clock::now();
+    CoefficientSet b = hweno_gpu::assemble_coefficients_parallel(g, p);
+    auto t2 = std::chrono::steady_clock::now();
+    const std::vector<WorkReal>* pa[14] = {&a.b, &a.lam, &a.w_re, &a.w_im, &a.bt_re, &a.bt_im, &a.c_re,
+                                           &a.c_im, &a.ath, &a.p_mix, &a.r_rad, &a.br_re, &a.br_im, &a.bprime};
+    const std::vector<WorkReal>* pb[14] = {&b.b, &b.lam, &b.w_re, &b.w_im, &b.bt_re, &b.bt_im, &b.c_re,
+                                           &b.c_im, &b.ath, &b.p_mix, &b.r_rad, &b.br_re, &b.br_im, &b.bprime};
+    long diff = 0;
+    for (int q = 0; q < 14; ++q)
+      diff += std::memcmp(pa[q]->data(), pb[q]->data(), pa[q]->size() * sizeof(WorkReal)) != 0;
+    diff += std::memcmp(a.cotth.data(), b.cotth.data(), a.cotth.size() * sizeof(WorkReal)) != 0;
+    diff += !(a.max_speed == b.max_speed);
+    const double ts = std::chrono::duration<double>(t1 - t0).count();
+    const double tp = std::chrono::duration<double>(t2 - t1).count();
+    std::printf("coefficients 2048x64: serial %.3f s, threaded %.3f s (%.1fx), planes differing %ld %s\n",
+                ts, tp, ts / tp, diff, diff == 0 ? "OK" : "FAIL");
+    bad += diff != 0;
+  }
+  // ---- §8f-3: checkpoint / restart through the GPU state (test_io.cpp:320-360)
+  {
+    RunConfig c = parse_config_text("[grid]\nnrho = 128\nntheta = 8\n[time]\ntau_end = 2\n", "inline");
+    const PhysicalParams& p = c.phys;
+    Grid g = make_grid(c.nrho, c.ntheta, p);
+    CoefficientSet cs = hweno_gpu::assemble_coefficients_parallel(g, p);
+    FieldLayout lay{g.nrho, g.ntheta};
+    WorkerPool pool(2);
+    WorkReal dt = select_dt(g, cs, c.stepper);
+    SampleHook none;
+    StateVec unbroken = initial_data(g, cs, p, c.init);
+    EvolutionRhs rref(g, cs, p, c.scheme, pool);
+    advance_steps(rref, c.stepper, unbroken, dt, 0, 30, none, pool);  // reference, unbroken
+    hweno_gpu::GpuEvolutionRhs gA(g, cs, p, c.scheme, device);
+    StateVec first = initial_data(g, cs, p, c.init);
+    hweno_gpu::advance_steps(gA, c.stepper, first, dt, 0, 15, none);
+    const std::string path =
+        (std::filesystem::temp_directory_path() / "hwg_dropin_restart.txt").string();
+    write_checkpoint(path, c, 15, WorkReal(15) * dt, lay, first);
+    Checkpoint cp = read_checkpoint(path, c, lay);
+    hweno_gpu::GpuEvolutionRhs gB(g, cs, p, c.scheme, device);
+    StateVec resumed = cp.state;
+    hweno_gpu::advance_steps(gB, c.stepper, resumed, dt, cp.step, 30, none);
+    long mism = 0;
+    for (int comp = 0; comp < kComponents; ++comp)
+      for (int j = 0; j < g.nrho; ++j)
+        for (int k = 0; k < g.ntheta; ++k)
+          mism += std::memcmp(&unbroken[lay.at(comp, j, k)], &resumed[lay.at(comp, j, k)],
+                              sizeof(WorkReal)) != 0;
+    std::printf("checkpoint at step 15 -> GPU restart -> step 30 vs unbroken reference: %ld values differ %s\n",
+                mism, mism == 0 ? "OK" : "FAIL");
+    bad += mism != 0;
+    std::filesystem::remove(path);
   }
   std::printf(bad ? "DROPIN FAIL\n" : "DROPIN OK\n");
   return bad ? 1 : 0;

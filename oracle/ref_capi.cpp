@@ -11,6 +11,7 @@
 //   advance_steps                          proj/src/evolve.cpp:237-265
 //   HorizonSampler / multipole_project     proj/src/diagnostics.cpp:128-283
 // No reference source is copied here; only its public headers are included.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -250,6 +251,67 @@ int ref_advance(void* hv, int stepper, double cfl, const double* dt_dd,
     stats[1] = rs.blew_up ? 1 : 0;
     stats[2] = rs.blowup_step;
     stats[3] = n_obs;
+    if (wall) *wall = rs.wall_seconds;
+  });
+}
+
+// A production-style run (driver.cpp:22-93 without files): initial data,
+// select_dt, steps_for, sample_stride, and advance_steps with the driver's
+// observer hook.  Per sample (row of 15): tau, phi, dphi1, dphi2, dphi3, obs
+// (state_sample at j_obs), proj (multipole_project of Psi_R, Psi_I at j_obs),
+// scri (state_sample at nrho-1); re/im pairs, .hi limbs.  k_obs = ntheta/2,
+// j_obs = nearest_rho_index(observer_rho).  stats: steps_done, blew_up,
+// blowup_step, n_obs, planned steps.
+int ref_run_series(void* hv, int ell, double center, double width, double amplitude,
+                   int stepper, double cfl, double tau_end, double cadence,
+                   double observer_rho, double* out, long max_rows, long* stats,
+                   double* wall) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    InitialDataSpec id;
+    id.ell = ell;
+    id.center = WorkReal(center);
+    id.width = WorkReal(width);
+    id.amplitude = WorkReal(amplitude);
+    StateVec u = initial_data(h->g, h->cs, h->p, id);
+    StepperSpec st;
+    st.kind = stepper == 0 ? StepperSpec::ssprk33 : StepperSpec::ssprk104;
+    st.cfl = WorkReal(cfl);
+    WorkReal dt = select_dt(h->g, h->cs, st);
+    const long steps = steps_for(dt, tau_end);
+    const FieldLayout& lay = h->rhs->layout();
+    const int kobs = h->g.ntheta / 2;
+    long jobs = std::lround((observer_rho - h->g.rho_min.hi) / h->g.drho.hi);
+    jobs = std::max(0L, std::min(jobs, long(h->g.nrho - 1)));
+    HorizonSampler hs(h->g, h->p, lay, kobs);
+    long n = 0;
+    SampleHook hook;
+    hook.every = sample_stride(dt, cadence);
+    hook.fn = [&](long, const WorkReal& tau, const StateVec& s) {
+      if (n >= max_rows) return;
+      double* r = out + 15 * n;
+      HorizonObservables ob = hs.sample(s);
+      CxW o = state_sample(s, lay, int(jobs), kobs);
+      CxW sc = state_sample(s, lay, lay.nrho - 1, kobs);
+      r[0] = tau.hi;
+      r[1] = ob.phi.re.hi; r[2] = ob.phi.im.hi;
+      for (int d = 0; d < 3; ++d) { r[3 + 2 * d] = ob.dphi[d].re.hi; r[4 + 2 * d] = ob.dphi[d].im.hi; }
+      r[9] = o.re.hi; r[10] = o.im.hi;
+      if (h->p.mmode == 0) {
+        r[11] = multipole_project(theta_slice(s, lay, 0, int(jobs)), h->p.spin, 0, ell).hi;
+        r[12] = multipole_project(theta_slice(s, lay, 1, int(jobs)), h->p.spin, 0, ell).hi;
+      } else {
+        r[11] = r[12] = 0.0;
+      }
+      r[13] = sc.re.hi; r[14] = sc.im.hi;
+      ++n;
+    };
+    RunStats rs = advance_steps(*h->rhs, st, u, dt, 0, steps, hook, *h->pool);
+    stats[0] = rs.steps_done;
+    stats[1] = rs.blew_up ? 1 : 0;
+    stats[2] = rs.blowup_step;
+    stats[3] = n;
+    stats[4] = steps;
     if (wall) *wall = rs.wall_seconds;
   });
 }
