@@ -72,7 +72,8 @@ struct StageArgs {
   int phys_lo, phys_hi;            // slab holds the excision / scri end
   int nranges;
   int negpar;                      // theta parity (-1)^(m+s) == -1
-  long long step;                  // blowup_step recorded if the scan fails
+  long long step;                  // blowup_step recorded if the scan fails; < 0: use flag[2]
+  int bump;                        // stage 0 in counter mode: flag[2] += 1 (graph replay)
   double eps4;                     // fp64 weights: 4 eps (scaled indicators)
   double eps;                      // fp64 weno3
   float epsf;                      // fp32 weights: eps demoted
@@ -337,8 +338,8 @@ struct Slot {
 };
 
 template <int EPI>
-constexpr size_t stage_smem_bytes() {
-  return (size_t)kWarpsPerBlock * Slot<EPI>::S * (Slot<EPI>::BYTES + 8);
+constexpr size_t stage_smem_bytes(int wpb = kWarpsPerBlock) {
+  return (size_t)wpb * Slot<EPI>::S * (Slot<EPI>::BYTES + 8);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -372,6 +373,7 @@ template <int SCH, int MODE, int EPI>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_MINB)
 stage_kernel(const StageArgs a) {
   if (a.flag != nullptr && *(volatile unsigned long long*)a.flag != 0ull) return;  // frozen
+  if (a.bump && blockIdx.x == 0 && threadIdx.x == 0) a.flag[2] += 1ull;  // step counter
   using Wn = Win<SCH>;
   using SlotT = Slot<EPI>;
   constexpr int SL = Wn::SL, PL = Wn::PL, R = Wn::R, SW = Wn::SW, PW = Wn::PW;
@@ -380,7 +382,8 @@ stage_kernel(const StageArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int gw = blockIdx.x * kWarpsPerBlock + wib;
+  const int wpb = blockDim.x >> 5;                     // warps per block (1, 2 or 4)
+  const int gw = blockIdx.x * wpb + wib;
   const int chunk = gw % a.nchunks;
   const int range = gw / a.nchunks;
   if (range >= a.nranges) return;                       // whole warp
@@ -403,7 +406,7 @@ stage_kernel(const StageArgs a) {
   const int wsrc = reflect_col(k, nt, wflip, a.negpar) - k0;
 
   unsigned char* ring = smem + (size_t)wib * S * SB;
-  const uint32_t bar0 = smem_u32(smem + (size_t)kWarpsPerBlock * S * SB) + wib * S * 8;
+  const uint32_t bar0 = smem_u32(smem + (size_t)wpb * S * SB) + wib * S * 8;
   const double2* xblk = a.x + chunk * kStateBlk;         // this chunk's block at row 0
   const double2* cblk = a.coef + chunk * kCoefBlk;
 
@@ -656,7 +659,7 @@ stage_kernel(const StageArgs a) {
     if (++slot == S) { slot = 0; parity ^= 1u; }
   }
   if (CHECK && __any_sync(kFull, bad) && lane == 0) {
-    atomicExch(a.flag + 1, (unsigned long long)a.step);
+    atomicExch(a.flag + 1, a.step >= 0 ? (unsigned long long)a.step : a.flag[2]);
     atomicOr(a.flag, 1ull);
   }
 }

@@ -8,11 +8,13 @@
 
 namespace hwg {
 // fp64 / mixed / linear tiers (stage_kernel)
-void launch_stage_fast(const StageArgs& a, int scheme, int mode, int epi, int blocks,
+void launch_stage_fast(const StageArgs& a, int scheme, int mode, int epi, int blocks, int wpb,
                        cudaStream_t stream);
-cudaError_t occupancy_fast(int* blocks_per_sm);
+cudaError_t occupancy_fast(int* blocks_per_sm);   // also sets every kernel's smem attribute
+void init_attributes_fast();
 // double-double tiers (stage_kernel_dd)
-void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks,
+void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks, int wpb,
                      cudaStream_t stream);
 cudaError_t occupancy_dd(int* blocks_per_sm);
+void init_attributes_dd();
 }  // namespace hwg

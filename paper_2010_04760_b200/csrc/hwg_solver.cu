@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -91,7 +92,6 @@ inline DD dd_div(DD a, DD b) {  // precision.hpp operator/
 }
 inline DD I(double v) { return {v, 0.0}; }
 inline DD Q(double num, double den) { return dd_div(I(num), I(den)); }
-inline double ddq(double num, double den) { return Q(num, den).hi; }
 inline dd to_dev(DD v) { return {v.hi, v.lo}; }
 }  // namespace
 
@@ -113,10 +113,20 @@ struct hwg_solver {
   int cur = 0, scr1 = 1, scr2 = 2, scr3 = 3, scr4 = 4;
   unsigned long long* flag = nullptr;
   unsigned long long* hflag = nullptr;  // pinned
-  int nchunks = 0, nranges = 0, blocks = 0;
+  int nchunks = 0, nranges = 0, blocks = 0, wpb = kWarpsPerBlock;
   double* stage_dev = nullptr;
   size_t stage_cap = 0;
   DD drho{0, 0}, dtheta{0, 0}, eps{0, 0}, sigma{0, 0};
+  // CUDA graphs of one register-rotation period (2 steps), keyed by stepper,
+  // dt and the rotation state at capture
+  struct GraphEntry {
+    int stepper;
+    double dt_hi, dt_lo;
+    int rot[5];
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = true;
   // observers
   int kobs = -1, j0 = -1, jobs = -1;
   double* obs_w = nullptr;   // 32 horizon weights + ntheta projection weights
@@ -272,7 +282,7 @@ int mode_of(const hwg_solver* s) {
 }
 
 int launch(hwg_solver* s, const StageArgs& a, int epi) {
-  launch_stage_fast(a, s->d.scheme, mode_of(s), epi, s->blocks, s->stream);
+  launch_stage_fast(a, s->d.scheme, mode_of(s), epi, s->blocks, s->wpb, s->stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     s->err = std::string("stage launch: ") + cudaGetErrorString(e);
@@ -282,7 +292,7 @@ int launch(hwg_solver* s, const StageArgs& a, int epi) {
 }
 
 int launch(hwg_solver* s, const StageArgsDD& a, int epi) {
-  launch_stage_dd(a, s->d.scheme, mode_of(s), epi, s->blocks, s->stream);
+  launch_stage_dd(a, s->d.scheme, mode_of(s), epi, s->blocks, s->wpb, s->stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     s->err = std::string("stage launch: ") + cudaGetErrorString(e);
@@ -419,13 +429,18 @@ Plan make_plan(const hwg_solver* s, int stepper, int stage, DD dt) {
   return p;
 }
 
+// step >= 0: the kernel records step + 1 on blow-up; step < 0: counter mode
+// (flag[2] is bumped by stage 0 and recorded by the scan) for graph replay
 int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, long long step) {
   const Plan p = make_plan(s, stepper, stage, DD{dt_hi, dt_lo});
+  const long long rec = step >= 0 ? step + 1 : -1;
+  const int bump = (step < 0 && stage == 0) ? 1 : 0;
   int rc;
   auto r0 = [&](int r) -> double2* { return r >= 0 ? row0(s, r) : nullptr; };
   if (s->ddm) {
     StageArgsDD a = base_args_dd(s);
-    a.step = step + 1;
+    a.step = rec;
+    a.bump = bump;
     a.x = r0(p.x); a.o = r0(p.out); a.ua = r0(p.ua); a.ub = r0(p.ub); a.ug = r0(p.ug);
     a.f = r0(p.f);
     a.k.ca = to_dev(p.ca); a.k.cb = to_dev(p.cb); a.k.cc = to_dev(p.cc);
@@ -433,7 +448,8 @@ int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, 
     rc = launch(s, a, p.epi);
   } else {
     StageArgs a = base_args(s);
-    a.step = step + 1;
+    a.step = rec;
+    a.bump = bump;
     a.x = r0(p.x); a.o = r0(p.out); a.ua = r0(p.ua); a.ub = r0(p.ub); a.ug = r0(p.ug);
     a.f = r0(p.f);
     a.ca = p.ca.hi; a.cb = p.cb.hi; a.cc = p.cc.hi; a.cg = p.cg.hi; a.cd = p.cd.hi; a.ce = p.ce.hi;
@@ -558,6 +574,73 @@ DD tau_of(long long step, double dt_hi, double dt_lo) {  // WorkReal(double(s)) 
   return dd_mul(I((double)step), {dt_hi, dt_lo});
 }
 
+__global__ void set_counter_kernel(unsigned long long* ctr, long long v) { *ctr = (unsigned long long)v; }
+
+bool graphs_ok(const hwg_solver* s) {
+  if (!s->use_graphs || s->stream == nullptr || s->stream == cudaStreamLegacy ||
+      s->stream == cudaStreamPerThread)
+    return false;
+  return true;
+}
+
+// nsteps whole steps from step_begin.  With graphs: the step counter is set
+// once, then each pair of steps (one rotation period) replays a cached graph.
+int launch_steps_impl(hwg_solver* s, int stepper, double dt_hi, double dt_lo, long long s0,
+                      long long nsteps) {
+  const int ns = stepper == HWG_SSPRK33 ? 3 : 10;
+  if (stepper == HWG_SSPRK104) {
+    int rc = ensure_regs(s, 5);
+    if (rc) return rc;
+  }
+  if (!graphs_ok(s) || nsteps < 2) {
+    for (long long q = 0; q < nsteps; ++q)
+      for (int st = 0; st < ns; ++st) {
+        int rc = do_stage(s, stepper, st, dt_hi, dt_lo, s0 + q);
+        if (rc) return rc;
+      }
+    return HWG_OK;
+  }
+  set_counter_kernel<<<1, 1, 0, s->stream>>>(s->flag + 2, s0);
+  CK(cudaGetLastError());
+  long long q = 0;
+  for (; q + 2 <= nsteps; q += 2) {
+    const int rot[5] = {s->cur, s->scr1, s->scr2, s->scr3, s->scr4};
+    cudaGraphExec_t exec = nullptr;
+    for (auto& e : s->graphs)
+      if (e.stepper == stepper && e.dt_hi == dt_hi && e.dt_lo == dt_lo &&
+          std::equal(rot, rot + 5, e.rot)) {
+        exec = e.exec;
+        break;
+      }
+    if (!exec) {
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+      int rc = HWG_OK;
+      for (int k = 0; k < 2 && rc == HWG_OK; ++k)
+        for (int st = 0; st < ns && rc == HWG_OK; ++st) rc = do_stage(s, stepper, st, dt_hi, dt_lo, -1);
+      cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
+      if (rc) return rc;
+      if (ce != cudaSuccess) {
+        s->err = std::string("graph capture: ") + cudaGetErrorString(ce);
+        return HWG_ECUDA;
+      }
+      CK(cudaGraphInstantiate(&exec, g, 0));
+      cudaGraphDestroy(g);
+      // the capture ran do_stage's host bookkeeping for 2 steps: the
+      // rotation is back where it started, as after a replay
+      hwg_solver::GraphEntry e{stepper, dt_hi, dt_lo, {rot[0], rot[1], rot[2], rot[3], rot[4]}, exec};
+      s->graphs.push_back(e);
+    }
+    CK(cudaGraphLaunch(exec, s->stream));
+  }
+  for (; q < nsteps; ++q)
+    for (int st = 0; st < ns; ++st) {
+      int rc = do_stage(s, stepper, st, dt_hi, dt_lo, -1);
+      if (rc) return rc;
+    }
+  return HWG_OK;
+}
+
 int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, const double* cotth,
                 const double* cot_lo, bool ddm, hwg_solver** out) {
   *out = nullptr;
@@ -609,6 +692,7 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   s->dtheta = {d->dtheta, ddm ? d->dtheta_lo : 0.0};
   s->eps = {d->eps, ddm ? d->eps_lo : 0.0};
   s->sigma = {d->sigma, ddm ? d->sigma_lo : 0.0};
+  if (const char* e = std::getenv("HWG_NO_GRAPH")) s->use_graphs = e[0] == '0';
   auto fail = [&](int rc) {
     g_create_err = s->err;
     hwg_destroy(s);
@@ -633,8 +717,8 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   CK(cudaMalloc(&s->coef, CB * sizeof(double2)));
   CK(cudaMemsetAsync(s->coef, 0, CB * sizeof(double2), s->stream));
   CK(cudaMalloc(&s->cot, 2 * s->ntp * sizeof(double)));
-  CK(cudaMalloc(&s->flag, 2 * sizeof(unsigned long long)));
-  CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
+  CK(cudaMalloc(&s->flag, 3 * sizeof(unsigned long long)));  // blown, blowup step, step counter
+  CK(cudaMemsetAsync(s->flag, 0, 3 * sizeof(unsigned long long), s->stream));
   CK(cudaMallocHost(&s->hflag, 2 * sizeof(unsigned long long)));
   CK(cudaMallocHost(&s->obs_host, 16 * sizeof(double)));
   CK(cudaMalloc(&s->obs_dev, 16 * sizeof(double)));
@@ -685,9 +769,15 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
     CK(ddm ? occupancy_dd(&occ) : occupancy_fast(&occ));
     const long long target = (long long)nsm * std::max(occ, 1) * kWarpsPerBlock;
     long long nr = std::max<long long>(1, target / s->nchunks);
-    nr = std::min<long long>(nr, std::max(1, s->n / 8));  // >= 8 rows per range
+    int minrows = 4;  // rows per range (the window warm-up costs ~2 rows of work)
+    if (const char* e = std::getenv("HWG_MIN_ROWS")) minrows = std::max(4, std::atoi(e));
+    nr = std::min<long long>(nr, std::max(1, s->n / minrows));
     s->nranges = (int)nr;
-    s->blocks = (int)((nr * s->nchunks + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    // small grids: fewer warps per block so the warps spread over all SMs
+    const long long warps = nr * s->nchunks;
+    s->wpb = kWarpsPerBlock;
+    while (s->wpb > 1 && warps / s->wpb < nsm) s->wpb /= 2;
+    s->blocks = (int)((warps + s->wpb - 1) / s->wpb);
   }
   CK(cudaStreamSynchronize(s->stream));
 #undef CK
@@ -725,6 +815,7 @@ void hwg_destroy(hwg_solver* s) {
   if (!s) return;
   cudaSetDevice(s->dev);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  for (auto& e : s->graphs) cudaGraphExecDestroy(e.exec);
   for (int i = 0; i < s->nreg; ++i) cudaFree(s->reg[i]);
   cudaFree(s->coef);
   cudaFree(s->cot);
@@ -793,13 +884,8 @@ int hwg_launch_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double
 
 int hwg_launch_steps(hwg_solver* s, int stepper, double dt_hi, double dt_lo,
                      long long step_begin, long long nsteps) {
-  const int ns = stepper == HWG_SSPRK33 ? 3 : 10;
-  for (long long q = 0; q < nsteps; ++q)
-    for (int st = 0; st < ns; ++st) {
-      int rc = hwg_launch_stage(s, stepper, st, dt_hi, dt_lo, step_begin + q);
-      if (rc) return rc;
-    }
-  return HWG_OK;
+  cudaSetDevice(s->dev);
+  return launch_steps_impl(s, stepper, dt_hi, dt_lo, step_begin, nsteps);
 }
 
 int hwg_stage_input(const hwg_solver* s, int stepper, int stage, int* reg) {
@@ -829,7 +915,7 @@ int hwg_status(hwg_solver* s, int* blew, long long* step, int clear) {
 int hwg_launch_info(const hwg_solver* s, int* blocks, int* threads, int* nranges, int* nchunks,
                     int* pitch) {
   *blocks = s->blocks;
-  *threads = kWarpsPerBlock * 32;
+  *threads = s->wpb * 32;
   *nranges = s->nranges;
   *nchunks = s->nchunks;
   *pitch = (int)s->rs;
@@ -880,7 +966,6 @@ int hwg_advance(hwg_solver* s, int stepper, double dt_hi, double dt_lo, long lon
   cudaSetDevice(s->dev);
   hwg_run_stats st{0, 0.0, 0, -1};
   if (every < 1) every = 1;
-  const int ns = stepper == HWG_SSPRK33 ? 3 : 10;
   const long long poll = 256;
   auto t0 = std::chrono::steady_clock::now();
   int rc = HWG_OK;
@@ -898,7 +983,8 @@ int hwg_advance(hwg_solver* s, int stepper, double dt_hi, double dt_lo, long lon
     }
     return HWG_OK;
   };
-  for (long long q = s0;; ++q) {
+  long long q = s0;
+  for (;;) {
     const bool hook_now = hook && (q % every == 0 || q == s0 || q == s1);
     if (hook_now || q == s1 || (q - s0) % poll == 0) {
       bool blown = false;
@@ -912,10 +998,13 @@ int hwg_advance(hwg_solver* s, int stepper, double dt_hi, double dt_lo, long lon
       hook(q, tau.hi, tau.lo, &ob, user);
     }
     if (q == s1) break;
-    for (int k = 0; k < ns && rc == HWG_OK; ++k) rc = hwg_launch_stage(s, stepper, k, dt_hi, dt_lo, q);
-    if (rc) break;
-    launched_to = q + 1;
+    // next stop: hook step, poll point or the end
+    long long next = std::min(s1, s0 + ((q - s0) / poll + 1) * poll);
+    if (hook) next = std::min(next, (q / every + 1) * every);
+    if ((rc = launch_steps_impl(s, stepper, dt_hi, dt_lo, q, next - q))) break;
+    launched_to = next;
     st.steps_done = launched_to - s0;
+    q = next;
   }
   cudaStreamSynchronize(s->stream);
   st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

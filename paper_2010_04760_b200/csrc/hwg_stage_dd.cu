@@ -6,26 +6,31 @@ namespace hwg {
 namespace {
 template <int SCH, int MODE, int EPI>
 struct DDLauncher {
-  static void run(const StageArgsDD& a, int blocks, cudaStream_t st) {
-    static bool attr = [] {
-      cudaFuncSetAttribute(stage_kernel_dd<SCH, MODE, EPI>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)stage_smem_bytes_dd<EPI>());
-      return true;
-    }();
-    (void)attr;
-    stage_kernel_dd<SCH, MODE, EPI><<<blocks, kWarpsPerBlock * 32, stage_smem_bytes_dd<EPI>(),
-                                      st>>>(a);
+  static void attr() {
+    cudaFuncSetAttribute(stage_kernel_dd<SCH, MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stage_smem_bytes_dd<EPI>());
+  }
+  static void run(const StageArgsDD& a, int blocks, int wpb, cudaStream_t st) {
+    stage_kernel_dd<SCH, MODE, EPI><<<blocks, wpb * 32, stage_smem_bytes_dd<EPI>(wpb), st>>>(a);
   }
 };
 }  // namespace
 
 void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks,
-                     cudaStream_t stream) {
-  dispatch<DDLauncher>(a, scheme, mode, epi, blocks, stream);
+                     int wpb, cudaStream_t stream) {
+  dispatch<DDLauncher>(a, scheme, mode, epi, blocks, wpb, stream);
+}
+
+void init_attributes_dd() {
+  static bool done = [] {
+    attr_all<DDLauncher>();
+    return true;
+  }();
+  (void)done;
 }
 
 cudaError_t occupancy_dd(int* occ) {
+  init_attributes_dd();
   cudaError_t e = cudaFuncSetAttribute(stage_kernel_dd<WENO5, F64, EPI_RK3>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)stage_smem_bytes_dd<EPI_RK3>());

@@ -6,25 +6,31 @@ namespace hwg {
 namespace {
 template <int SCH, int MODE, int EPI>
 struct FastLauncher {
-  static void run(const StageArgs& a, int blocks, cudaStream_t st) {
-    static bool attr = [] {
-      cudaFuncSetAttribute(stage_kernel<SCH, MODE, EPI>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)stage_smem_bytes<EPI>());
-      return true;
-    }();
-    (void)attr;
-    stage_kernel<SCH, MODE, EPI><<<blocks, kWarpsPerBlock * 32, stage_smem_bytes<EPI>(), st>>>(a);
+  static void attr() {
+    cudaFuncSetAttribute(stage_kernel<SCH, MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)stage_smem_bytes<EPI>());
+  }
+  static void run(const StageArgs& a, int blocks, int wpb, cudaStream_t st) {
+    stage_kernel<SCH, MODE, EPI><<<blocks, wpb * 32, stage_smem_bytes<EPI>(wpb), st>>>(a);
   }
 };
 }  // namespace
 
 void launch_stage_fast(const StageArgs& a, int scheme, int mode, int epi, int blocks,
-                       cudaStream_t stream) {
-  dispatch<FastLauncher>(a, scheme, mode, epi, blocks, stream);
+                       int wpb, cudaStream_t stream) {
+  dispatch<FastLauncher>(a, scheme, mode, epi, blocks, wpb, stream);
+}
+
+void init_attributes_fast() {
+  static bool done = [] {
+    attr_all<FastLauncher>();
+    return true;
+  }();
+  (void)done;
 }
 
 cudaError_t occupancy_fast(int* occ) {
+  init_attributes_fast();
   cudaError_t e = cudaFuncSetAttribute(stage_kernel<WENO5, F64, EPI_RK3>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)stage_smem_bytes<EPI_RK3>());
