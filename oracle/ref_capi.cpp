@@ -23,6 +23,7 @@
 #include "hweno/diagnostics.hpp"
 #include "hweno/evolve.hpp"
 #include "hweno/geometry.hpp"
+#include "hweno/io.hpp"
 #include "hweno/parallel.hpp"
 #include "hweno/timestep.hpp"
 
@@ -313,6 +314,61 @@ int ref_run_series(void* hv, int ell, double center, double width, double amplit
     stats[3] = n;
     stats[4] = steps;
     if (wall) *wall = rs.wall_seconds;
+  });
+}
+
+// execute_run's setup from an INI text (parse_config_text, io.cpp), then the
+// same observer hook as ref_run_series.  workers overrides [parallel].
+int ref_run_config(const char* ini, int workers, double* out, long max_rows, long* stats,
+                   double* wall, double* dt_out) {
+  return guarded([&] {
+    RunConfig cfg = parse_config_text(ini, "inline");
+    auto h = std::make_unique<RefHandle>();
+    h->p = cfg.phys;
+    h->g = make_grid(cfg.nrho, cfg.ntheta, h->p);
+    h->cs = assemble_coefficients(h->g, h->p);
+    h->spec = cfg.scheme;
+    h->pool = std::make_unique<WorkerPool>(workers > 0 ? workers : cfg.workers);
+    h->rhs = std::make_unique<EvolutionRhs>(h->g, h->cs, h->p, h->spec, *h->pool);
+    StateVec u = initial_data(h->g, h->cs, h->p, cfg.init);
+    WorkReal dt = select_dt(h->g, h->cs, cfg.stepper);
+    const long steps = steps_for(dt, cfg.tau_end);
+    const FieldLayout& lay = h->rhs->layout();
+    const int kobs = cfg.ntheta / 2;
+    long jobs = std::lround((to_double(cfg.output.observer_rho) - h->g.rho_min.hi) / h->g.drho.hi);
+    jobs = std::max(0L, std::min(jobs, long(h->g.nrho - 1)));
+    HorizonSampler hs(h->g, h->p, lay, kobs);
+    long n = 0;
+    SampleHook hook;
+    hook.every = sample_stride(dt, cfg.output.series_cadence);
+    hook.fn = [&](long, const WorkReal& tau, const StateVec& s) {
+      if (n >= max_rows) return;
+      double* r = out + 15 * n;
+      HorizonObservables ob = hs.sample(s);
+      CxW o = state_sample(s, lay, int(jobs), kobs);
+      CxW sc = state_sample(s, lay, lay.nrho - 1, kobs);
+      r[0] = tau.hi;
+      r[1] = ob.phi.re.hi; r[2] = ob.phi.im.hi;
+      for (int d = 0; d < 3; ++d) { r[3 + 2 * d] = ob.dphi[d].re.hi; r[4 + 2 * d] = ob.dphi[d].im.hi; }
+      r[9] = o.re.hi; r[10] = o.im.hi;
+      if (h->p.mmode == 0) {
+        r[11] = multipole_project(theta_slice(s, lay, 0, int(jobs)), h->p.spin, 0, cfg.init.ell).hi;
+        r[12] = multipole_project(theta_slice(s, lay, 1, int(jobs)), h->p.spin, 0, cfg.init.ell).hi;
+      } else {
+        r[11] = r[12] = 0.0;
+      }
+      r[13] = sc.re.hi; r[14] = sc.im.hi;
+      ++n;
+    };
+    RunStats rs = advance_steps(*h->rhs, cfg.stepper, u, dt, 0, steps, hook, *h->pool);
+    stats[0] = rs.steps_done;
+    stats[1] = rs.blew_up ? 1 : 0;
+    stats[2] = rs.blowup_step;
+    stats[3] = n;
+    stats[4] = steps;
+    if (wall) *wall = rs.wall_seconds;
+    dt_out[0] = dt.hi;
+    dt_out[1] = dt.lo;
   });
 }
 

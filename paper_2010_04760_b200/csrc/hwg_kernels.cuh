@@ -287,7 +287,11 @@ template <int SCH>
 struct Win {
   // register windows, rows j - L .. j + R (L + R >= 4 so the cubic scri
   // continuation always has its four predecessors in registers)
+#ifdef HWG_UNROLL
+  static constexpr int SL = (SCH == FD6KO) ? 4 : 2;  // Psi (same width as pi: one period)
+#else
   static constexpr int SL = (SCH == FD6KO) ? 4 : (SCH == WENO5 ? 1 : 2);  // Psi
+#endif
   static constexpr int PL = (SCH == FD6KO) ? 4 : 2;                       // pi
   static constexpr int R = (SCH == FD6KO) ? 4 : (SCH == WENO5 ? 3 : 2);
   static constexpr int SW = SL + R + 1, PW = PL + R + 1;
@@ -490,6 +494,10 @@ stage_kernel(const StageArgs a) {
   double2 hn = has_h ? ld2(hrow) : make_double2(0.0, 0.0);
   int slot = 0;
   uint32_t parity = 0;
+#ifdef HWG_UNROLL
+  constexpr int kUnroll = HWG_UNROLL;
+#pragma unroll kUnroll
+#endif
   for (int j = jb; j < je; ++j) {
     const unsigned char* sl = ring + (size_t)slot * SB;
     const double2* sd = reinterpret_cast<const double2*>(sl) + lane;
@@ -547,6 +555,9 @@ stage_kernel(const StageArgs a) {
     if (pole_chunk) {  // warp-uniform
       double2 img = make_double2(__shfl_sync(kFull, ps.x, wsrc & 31),
                                  __shfl_sync(kFull, ps.y, wsrc & 31));
+      // image column in the previous chunk (last chunk with one column)
+      if (!active && (wsrc < 0 || wsrc > 31))
+        img = ld2(a.x + (ptrdiff_t)j * rs + psi_off(k0 + wsrc));
       if (!active) wv = wflip ? neg2(img) : img;
     }
     const double2 su2 = shfl_up2(wv, 2), su1 = shfl_up2(wv, 1);

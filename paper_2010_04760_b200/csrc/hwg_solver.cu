@@ -105,6 +105,7 @@ struct hwg_solver {
   int sblk = kStateBlk;      // double2 per (row, chunk) state block
   int cblk = kCoefBlk;       // double2 per (row, chunk) coefficient block
   double2* coef = nullptr;   // coefficient blocks
+  DDConsts* kdev = nullptr;  // DD tiers: the reference's DD constants, device copy
   double* cot = nullptr;     // cot(theta) (fp64, or dd pairs), padded to nchunks*32
   double2* reg[5] = {};      // state registers, blocked layout incl. halo rows
   int nreg = 0;
@@ -337,6 +338,7 @@ StageArgsDD base_args_dd(const hwg_solver* s) {
   a.cot = reinterpret_cast<const dd*>(s->cot);
   a.coef = s->coef;
   a.flag = s->flag;
+  a.kdev = s->kdev;
   DDConsts& K = a.k;
   K.c1312 = to_dev(Q(13, 12));
   K.quarter = to_dev(Q(1, 4));
@@ -762,6 +764,11 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
     int rc = ensure_regs(s, 3);
     if (rc) return fail(rc);
   }
+  if (ddm) {
+    CK(cudaMalloc(&s->kdev, sizeof(DDConsts)));
+    const DDConsts k = base_args_dd(s).k;
+    CK(cudaMemcpy(s->kdev, &k, sizeof(DDConsts), cudaMemcpyHostToDevice));
+  }
   // launch geometry: one wave of warps, rho ranges balanced per theta chunk
   {
     int nsm = 148, occ = 1;
@@ -818,6 +825,7 @@ void hwg_destroy(hwg_solver* s) {
   for (auto& e : s->graphs) cudaGraphExecDestroy(e.exec);
   for (int i = 0; i < s->nreg; ++i) cudaFree(s->reg[i]);
   cudaFree(s->coef);
+  cudaFree(s->kdev);
   cudaFree(s->cot);
   cudaFree(s->flag);
   cudaFree(s->stage_dev);

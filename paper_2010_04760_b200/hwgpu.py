@@ -13,7 +13,6 @@ the built library raises.
 from __future__ import annotations
 
 import ctypes as C
-import math
 import os
 from dataclasses import dataclass
 
@@ -311,13 +310,9 @@ class GpuEvolution:
         self._chk(_lib.hwg_synchronize(self.h))
 
 
-def stage_bytes(stepper: str) -> float:
-    """Algorithmic HBM bytes per grid point per stage:
-    fp64 state 32 B per register touched + 9 fp64 coefficient planes (72 B)."""
-    if stepper == "ssprk33":
-        return (136 + 168 + 168) / 3.0
-    return 1520 / 10.0
-
-
-def dd_div(a: float, b: float) -> float:
-    return a / b if math.isfinite(a) else a
+def stage_bytes(stepper: str, mode: str = "mixed") -> float:
+    """Algorithmic HBM bytes per grid point per stage: fp64
+    state 32 B per register touched + 9 fp64 coefficient planes (72 B); the
+    double-double tiers move twice that."""
+    b = (136 + 168 + 168) / 3.0 if stepper == "ssprk33" else 1520 / 10.0
+    return 2 * b if mode.startswith("dd") else b

