@@ -343,7 +343,11 @@ struct Slot {
 
 template <int EPI>
 constexpr size_t stage_smem_bytes(int wpb = kWarpsPerBlock) {
+#ifdef HWG_SMEM_THETA
+  return (size_t)wpb * Slot<EPI>::S * (Slot<EPI>::BYTES + 8) + (size_t)wpb * 36 * 16;
+#else
   return (size_t)wpb * Slot<EPI>::S * (Slot<EPI>::BYTES + 8);
+#endif
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -560,6 +564,15 @@ stage_kernel(const StageArgs a) {
         img = ld2(a.x + (ptrdiff_t)j * rs + psi_off(k0 + wsrc));
       if (!active) wv = wflip ? neg2(img) : img;
     }
+#ifdef HWG_SMEM_THETA
+    // the chunk's extended row E[i] = Psi(k0 - 2 + i), i < 36, in shared memory
+    double2* trow = reinterpret_cast<double2*>(smem + (size_t)wpb * S * (SB + 8)) + wib * 36;
+    trow[lane + 2] = wv;
+    if (lane < 2) trow[lane] = h;
+    else if (lane >= 30) trow[lane + 4] = h;
+    __syncwarp();
+    const double2 m2 = trow[lane], m1 = trow[lane + 1], p1 = trow[lane + 3], p2 = trow[lane + 4];
+#else
     const double2 su2 = shfl_up2(wv, 2), su1 = shfl_up2(wv, 1);
     const double2 sd1 = shfl_dn2(wv, 1), sd2 = shfl_dn2(wv, 2);
     const double2 hd1 = shfl_dn2(h, 1), hu1 = shfl_up2(h, 1);
@@ -567,6 +580,7 @@ stage_kernel(const StageArgs a) {
     const double2 m1 = lane >= 1 ? su1 : hd1;
     const double2 p1 = lane <= 30 ? sd1 : hu1;
     const double2 p2 = lane <= 29 ? sd2 : h;
+#endif
     const double d1R = fma(8.0, p1.x - m1.x, m2.x - p2.x) * a.inv1;
     const double d1I = fma(8.0, p1.y - m1.y, m2.y - p2.y) * a.inv1;
     const double d2R = fma(-30.0, ps.x, fma(16.0, m1.x + p1.x, -(m2.x + p2.x))) * a.inv2;
