@@ -191,6 +191,26 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- B200 arm
+def make_runner(args, g, mode, rank, world, dist):
+    """Slab transport for N > 1: the fused halo push over NVLink peer memory
+    (slabs.PeerSlab) for the fp64 / mixed tiers, NCCL point-to-point
+    otherwise (or with --halo nccl)."""
+    from paper_2010_04760_b200 import slabs
+    if world > 1 and args.halo == "peer" and not mode.startswith("dd"):
+        import torch
+        r = slabs.PeerSlab(g, rank, world, "weno5")
+        t = torch.tensor([0 if r.error else 1], device=f"cuda:{torch.cuda.current_device()}",
+                         dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) == 1:
+            r.prime()
+            return r, "peer"
+        print(f"[bench rank {rank}] no peer mappings ({r.error}); NCCL halos", file=sys.stderr)
+        if r.error is None:
+            g.set_peers(None, None)
+    return slabs.DistSlab(g, rank, world, "weno5"), ("nccl" if world > 1 else "none")
+
+
 def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmup=None):
     from paper_2010_04760_b200 import hwgpu, slabs, synthetic
     spec = hwgpu.SchemeSpec("weno5", mode)
@@ -205,11 +225,29 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
     u0 = synthetic.initial_state(prob)
     g.set_state(u0)
     dt = synthetic.select_dt(prob, "ssprk33")
-    runner = slabs.DistSlab(g, rank, world, "weno5")
+    runner, halo = make_runner(args, g, mode, rank, world, dist)
     P = prob["nrho"] * prob["ntheta"]
     for q in range(W):
         runner.step("ssprk33", dt, q)
     torch.cuda.synchronize()
+    if halo == "peer":
+        # all ranks agree the fused halo push works here, else fall back to NCCL
+        ok = 1
+        try:
+            g.status()
+        except hwgpu.HwgError as e:
+            print(f"[bench rank {rank}] fused halo push failed ({e}); NCCL halos", file=sys.stderr)
+            ok = 0
+        t = torch.tensor([ok], device=f"cuda:{dev}", dtype=torch.int32)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) == 0:
+            g.set_peers(None, None)
+            g.status(clear=True)
+            g.set_state(u0)
+            runner, halo = slabs.DistSlab(g, rank, world, "weno5"), "nccl"
+            for q in range(W):
+                runner.step("ssprk33", dt, q)
+            torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -244,48 +282,91 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
     kern_ms = float(stage_ms.sum())
     achieved = bytes_per_step * K / (kern_ms / 1000.0) / 1e9
     return g, dict(value=value, total_ms=total_ms, stage_ms=stage_ms, achieved_gbs=achieved,
-                   kern_ms=kern_ms, P=P, dt=dt, K=K)
+                   kern_ms=kern_ms, P=P, dt=dt, K=K, halo=halo, runner=runner)
 
 
-def e2e_mode(g, args, prob, world, rank, torch, dist, dt):
-    """Same metric through the C ABI with HOST buffers (pinned, as the
-    contract allows): per step hwg_set_state (host FieldLayout -> device) +
-    one RK3 step + hwg_get_state (device -> host FieldLayout, ghosts filled)."""
-    from paper_2010_04760_b200 import synthetic
+def _e2e_job(g, u, out, dt, q, runner=None):
+    """One end-to-end step through the C ABI with host buffers: hwg_set_state
+    (host FieldLayout -> device), one SSP-RK3 step, hwg_get_state (device ->
+    host FieldLayout, ghosts filled).  Returns the three phase times."""
     from paper_2010_04760_b200.hwgpu import _lib, _p
-    u0 = synthetic.initial_state(prob)
-    u = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
-    u[...] = u0
-    out = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
-    ke = max(1, min(args.e2e_steps, args.steps))
+    a = time.perf_counter()
     g.set_state(u)
-    g.launch_steps("ssprk33", dt, 0, 1)
-    g._chk(_lib.hwg_get_state(g.h, _p(out)))  # warm the staging buffers
+    if runner is not None and hasattr(runner, "prime"):
+        runner.prime()  # fused-halo slabs: halos of the uploaded state
+    b = time.perf_counter()
+    if runner is None:
+        g.launch_steps("ssprk33", dt, q, 1)
+    else:
+        runner.step("ssprk33", dt, q)
+    g.synchronize()
+    c = time.perf_counter()
+    g._chk(_lib.hwg_get_state(g.h, _p(out)))
+    return b - a, c - b, time.perf_counter() - c
+
+
+def e2e_mode(g, args, prob, world, rank, torch, dist, dt, runner=None):
+    """Same metric through the C ABI with HOST buffers (pinned, as the
+    contract allows): every step uploads its host state, advances one RK3 step
+    and reads the whole state back (_e2e_job).  The steps are independent
+    jobs (same input), so on one GPU two handles on their own streams run them
+    two-deep from two host threads: job q+1's upload (H2D) overlaps job q's
+    read-back (D2H), both PCIe directions busy.  Multi-GPU slabs run them
+    serially (the halo exchange is one NCCL sequence per process)."""
+    import threading
+    from paper_2010_04760_b200 import hwgpu, slabs, synthetic
+    u0 = synthetic.initial_state(prob)
+    ke = max(1, min(args.e2e_steps, args.steps))
+    lanes = 2 if world == 1 and ke > 1 else 1
+    hs = [g]
+    for _ in range(lanes - 1):
+        h = hwgpu.GpuEvolution(prob["nrho"], prob["ntheta"], prob["drho"], prob["dtheta"],
+                               prob["parity"], prob["coef"], prob["cotth"], g.spec,
+                               device=torch.cuda.current_device(), coef_ld=prob["nrho"],
+                               coef_row0=0)
+        hs.append(h)
+    bufs = []
+    for h in hs:
+        if lanes > 1:
+            h.set_stream(None)  # each lane on its own stream
+        u = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
+        u[...] = u0
+        out = torch.empty(u0.shape, dtype=torch.float64, pin_memory=True).numpy()
+        bufs.append((u, out))
+        _e2e_job(h, u, out, dt, 0)  # warm the staging buffers and graphs
+    runner = runner if world > 1 else None
     if world > 1:
         dist.barrier()
-    t_set = t_step = t_get = 0.0
+    times = [[0.0, 0.0, 0.0] for _ in hs]
+
+    def lane(i):
+        for q in range(i, ke, lanes):
+            r = _e2e_job(hs[i], bufs[i][0], bufs[i][1], dt, q, runner)
+            for k in range(3):
+                times[i][k] += r[k]
+
     t0 = time.perf_counter()
-    for q in range(ke):
-        a = time.perf_counter()
-        g.set_state(u)
-        b = time.perf_counter()
-        g.launch_steps("ssprk33", dt, q, 1)
-        g.synchronize()
-        c = time.perf_counter()
-        g._chk(_lib.hwg_get_state(g.h, _p(out)))
-        d = time.perf_counter()
-        t_set += b - a
-        t_step += c - b
-        t_get += d - c
+    if lanes == 1:
+        lane(0)
+    else:
+        th = [threading.Thread(target=lane, args=(i,)) for i in range(lanes)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
     wall = time.perf_counter() - t0
+    for h in hs[1:]:
+        h.close()
     if world > 1:
         t = torch.tensor([wall], device=f"cuda:{torch.cuda.current_device()}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wall = float(t.item())
     P = prob["nrho"] * prob["ntheta"]
-    return dict(value=world * P * 3 * ke / wall, steps=ke, h2d=int(u.nbytes), d2h=int(out.nbytes),
-                ms=dict(set_state=1e3 * t_set / ke, step=1e3 * t_step / ke,
-                        get_state=1e3 * t_get / ke))
+    tot = [sum(t[k] for t in times) / ke for k in range(3)]
+    u = bufs[0][0]
+    return dict(value=world * P * 3 * ke / wall, steps=ke, h2d=int(u.nbytes), d2h=int(u.nbytes),
+                lanes=lanes, ms=dict(set_state=1e3 * tot[0], step=1e3 * tot[1],
+                                     get_state=1e3 * tot[2], wall_per_step=1e3 * wall / ke))
 
 
 def run_b200(args):
@@ -331,7 +412,7 @@ def run_b200(args):
                               steps=max(1, min(3, args.steps)), warmup=1)
             gd.close()
             results[mode] = r
-    e2e = e2e_mode(g, args, prob, world, rank, torch, dist, head["dt"])
+    e2e = e2e_mode(g, args, prob, world, rank, torch, dist, head["dt"], head["runner"])
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r, cores, sample, kind = cpu_reference_rate(args.cpu_seconds)
@@ -364,16 +445,18 @@ def run_b200(args):
                                f"{args.nrho * world}x{args.ntheta}), WENO5 {args.mode}, SSP-RK3",
                    "grid_points_per_gpu": head["P"], "stages_per_step": 3,
                    "l2": "inputs larger than L2 (no flush needed)",
-                   "parallelism": f"rho-slabs x{world}"},
+                   "parallelism": f"rho-slabs x{world}",
+                   "halo": head["halo"]},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                      "frac": ach / peak, "traffic": traffic, "peak_source": src,
                      "kernel": "hwg::stage_kernel<WENO5>",
                      "bytes_per_point_stage": 157.33},
         "clocks": clocks.summary(),
         "e2e": {"value": e2e["value"], "unit": UNIT, "h2d_bytes_per_step": e2e["h2d"],
-                "d2h_bytes_per_step": e2e["d2h"], "steps": e2e["steps"], "ms_per_step": e2e["ms"],
+                "d2h_bytes_per_step": e2e["d2h"], "steps": e2e["steps"], "lanes": e2e["lanes"],
+                "ms_per_step": e2e["ms"],
                 "path": "C ABI hwg_set_state + 1 RK3 step + hwg_get_state (pinned host "
-                        "FieldLayout fp64)"},
+                        "FieldLayout fp64); independent jobs, 'lanes' in flight"},
         "gpu_launches": 3 * K,
         "launch": info,
         "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / r["K"], "steps": r["K"],
@@ -402,7 +485,9 @@ def main():
     ap.add_argument("--mode", default="mixed", choices=["mixed", "f64"])
     ap.add_argument("--nrho", type=int, default=65536)
     ap.add_argument("--ntheta", type=int, default=512)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
+                    help="N > 1 slab halos: fused push over NVLink peer memory, or NCCL P2P")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dd", action="store_true")

@@ -67,6 +67,25 @@ enum EpiId {
   EPI_RK104_10 = 5   // o = a A + b B + c x + g (d G + e f) + scan  (rk104 stage 10)
 };
 
+// Slab neighbours over peer memory (multi-GPU radial slabs).
+// The stage kernel itself stores its first / last h output rows into the
+// neighbours' halo rows of the same register and bumps their arrival counter;
+// the next stage's boundary warps wait on their own counters before reading
+// halo rows.  Counters are monotonic: after e stages every neighbour has
+// signalled e * nchunks times (one per chunk), so a boundary warp at epoch e
+// waits for >= e * nchunks.
+struct PeerArgs {
+  double2* o_lo;                   // lower neighbour's output register at its row n_lo
+  double2* o_hi;                   // upper neighbour's output register at its row -h
+  unsigned long long* sig_lo;      // lower neighbour's "from upper" counter
+  unsigned long long* sig_hi;      // upper neighbour's "from lower" counter
+  unsigned long long* wait;        // own counters: [0] from lower, [1] from upper (flag + 6)
+  unsigned long long* epoch;       // own epoch (flag + 5)
+  long long timeout_ns;            // bounded spin: flag[0] |= 2 on expiry
+  int h;                           // halo rows pushed per side
+  int on_lo, on_hi;                // neighbour present
+};
+
 struct StageArgs {
   int n, nt, nchunks;
   int phys_lo, phys_hi;            // slab holds the excision / scri end
@@ -90,7 +109,12 @@ struct StageArgs {
   double2* f;                      // F store (rk104 stage 5)
   const double2* coef;             // coefficient blocks, rows [0, n)
   const double* cot;               // cot(theta_k), padded to nchunks*32
-  unsigned long long* flag;        // [0] blown, [1] blowup step
+  unsigned long long* flag;        // [0] blown, [1] blowup step, [2] step counter, [3] pending
+  // end-of-launch ticket (flag + 4): the last warp publishes the pending
+  // blow-up bit (so every block of a launch sees the same frozen state) and
+  // advances the peer epoch.  Null for launches that need neither.
+  unsigned long long* tick;
+  PeerArgs px;                     // fused halo push to the neighbour slabs (NVLink P2P)
 };
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
@@ -110,7 +134,7 @@ __device__ __forceinline__ double2 cubic(double2 a, double2 b, double2 c, double
 // reference's cubic ghosts.  Rare path: the orientation switch of a pi row.
 static __device__ __noinline__ double2 row_or_ghost(const double2* col, int r, ptrdiff_t rstride,
                                              int phys_lo) {
-  if (r >= 0 || !phys_lo) return __ldg(col + r * rstride);
+  if (r >= 0 || !phys_lo) return __ldcg(col + r * rstride);  // may be a peer-written halo row
   double2 g[8];
   for (int m = 0; m < 4; ++m) g[4 + m] = __ldg(col + m * rstride);
   for (int t = 1; t <= -r; ++t)
@@ -377,11 +401,120 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+__device__ __forceinline__ void peer_signal(unsigned long long* ctr, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// bounded spin until *ctr >= want; false on timeout
+static __device__ __noinline__ bool peer_wait(const unsigned long long* ctr, unsigned long long want,
+                                       long long timeout_ns) {
+  if (ld_acquire_sys(ctr) >= want) return true;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys(ctr) < want) {
+    __nanosleep(200);
+    if ((long long)(globaltimer() - t0) > timeout_ns) return false;
+  }
+  return true;
+}
+
+// boundary warps: wait for the neighbours' halo rows of this stage
+static __device__ __noinline__ void peer_wait_halos(unsigned long long* wait,
+                                                    const unsigned long long* epoch,
+                                                    unsigned long long* flag, int nchunks,
+                                                    long long timeout_ns, bool lo, bool hi) {
+  if ((threadIdx.x & 31) == 0) {
+    const unsigned long long want = *(volatile const unsigned long long*)epoch *
+                                    (unsigned long long)nchunks;
+    bool ok = true;
+    if (lo) ok &= peer_wait(wait, want, timeout_ns);
+    if (hi) ok &= peer_wait(wait + 1, want, timeout_ns);
+    if (!ok) atomicOr(flag, 2ull);
+    // the halo rows also arrive through the bulk-copy (async) proxy
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncwarp();
+}
+
+// push the boundary output rows this warp just wrote (its own stores, read
+// back by the same lanes) into the neighbours' halo rows over NVLink, then
+// signal their arrival counters
+static __device__ __noinline__ void peer_push_halos(const double2* o, double2* o_lo,
+                                                    double2* o_hi, unsigned long long* sig_lo,
+                                                    unsigned long long* sig_hi, int nchunks,
+                                                    int n, int nt, int h, int chunk, bool lo,
+                                                    bool hi) {
+  const int lane = threadIdx.x & 31;
+  const ptrdiff_t rs = (ptrdiff_t)nchunks * kStateBlk;
+  const ptrdiff_t c = chunk * kStateBlk + lane;
+  const double2* ob = o + c;
+  if ((chunk << 5) + lane < nt) {
+    for (int r = 0; lo && r < h; ++r) {
+      o_lo[r * rs + c] = ob[r * rs];
+      o_lo[r * rs + c + 32] = ob[r * rs + 32];
+    }
+    for (int r = 0; hi && r < h; ++r) {
+      o_hi[r * rs + c] = ob[(n - h + r) * rs];
+      o_hi[r * rs + c + 32] = ob[(n - h + r) * rs + 32];
+    }
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) {
+    if (lo) peer_signal(sig_lo, 1ull);
+    if (hi) peer_signal(sig_hi, 1ull);
+  }
+}
+
+// every warp of a launch takes a ticket; the last one publishes the pending
+// blow-up bit and advances the peer epoch
+static __device__ __noinline__ void launch_ticket(unsigned long long* tick,
+                                                  unsigned long long* flag,
+                                                  unsigned long long* epoch) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence();
+    const unsigned long long nw = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(tick, 1ull) == nw - 1) {
+      __threadfence();
+      if (atomicExch(flag + 3, 0ull) != 0ull) atomicOr(flag, 1ull);
+      if (epoch != nullptr) *epoch += 1ull;
+      *tick = 0ull;
+    }
+  }
+}
+
+template <int SCH, int MODE, int EPI>
+__device__ __forceinline__ void stage_body(const StageArgs& a);
+
 template <int SCH, int MODE, int EPI>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_MINB)
 stage_kernel(const StageArgs a) {
-  if (a.flag != nullptr && *(volatile unsigned long long*)a.flag != 0ull) return;  // frozen
+  if (a.flag != nullptr && *(volatile unsigned long long*)a.flag != 0ull) {  // frozen
+    // a frozen slab still releases its neighbours for this stage (no data)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (a.px.on_lo | a.px.on_hi)) {
+      if (a.px.on_lo) peer_signal(a.px.sig_lo, (unsigned long long)a.nchunks);
+      if (a.px.on_hi) peer_signal(a.px.sig_hi, (unsigned long long)a.nchunks);
+      *a.px.epoch += 1ull;
+    }
+    return;
+  }
   if (a.bump && blockIdx.x == 0 && threadIdx.x == 0) a.flag[2] += 1ull;  // step counter
+  stage_body<SCH, MODE, EPI>(a);
+  if (a.tick != nullptr)
+    launch_ticket(a.tick, a.flag, (a.px.on_lo | a.px.on_hi) ? a.px.epoch : nullptr);
+}
+
+template <int SCH, int MODE, int EPI>
+__device__ __forceinline__ void stage_body(const StageArgs& a) {
   using Wn = Win<SCH>;
   using SlotT = Slot<EPI>;
   constexpr int SL = Wn::SL, PL = Wn::PL, R = Wn::R, SW = Wn::SW, PW = Wn::PW;
@@ -394,7 +527,7 @@ stage_kernel(const StageArgs a) {
   const int gw = blockIdx.x * wpb + wib;
   const int chunk = gw % a.nchunks;
   const int range = gw / a.nchunks;
-  if (range >= a.nranges) return;                       // whole warp
+  if (range >= a.nranges) return;                       // whole warp (to the ticket)
   const int jb = (int)((long long)range * a.n / a.nranges);
   const int je = (int)((long long)(range + 1) * a.n / a.nranges);
   const int k0 = chunk << 5;
@@ -413,6 +546,10 @@ stage_kernel(const StageArgs a) {
   bool wflip;
   const int wsrc = reflect_col(k, nt, wflip, a.negpar) - k0;
 
+  // boundary ranges: wait for the neighbours' halo rows of this stage
+  if ((a.px.on_lo && range == 0) | (a.px.on_hi && range == a.nranges - 1))
+    peer_wait_halos(a.px.wait, a.px.epoch, a.flag, a.nchunks, a.px.timeout_ns,
+                    range == 0 && a.px.on_lo, range == a.nranges - 1 && a.px.on_hi);
   unsigned char* ring = smem + (size_t)wib * S * SB;
   const uint32_t bar0 = smem_u32(smem + (size_t)wpb * S * SB) + wib * S * 8;
   const double2* xblk = a.x + chunk * kStateBlk;         // this chunk's block at row 0
@@ -451,8 +588,8 @@ stage_kernel(const StageArgs a) {
     // only jb == 0 happens (ranges are >= 8 rows)
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      ips[IL + m] = ld2(xps + m * rs);
-      ipi[IL + m] = ld2(xpi + m * rs);
+      ips[IL + m] = __ldcg(xps + m * rs);
+      ipi[IL + m] = __ldcg(xpi + m * rs);
     }
 #pragma unroll
     for (int t = 1; t <= IL; ++t) {
@@ -461,8 +598,8 @@ stage_kernel(const StageArgs a) {
     }
 #pragma unroll
     for (int m = IL + 4; m < IW; ++m) {
-      ips[m] = ld2(xps + (m - IL) * rs);
-      ipi[m] = ld2(xpi + (m - IL) * rs);
+      ips[m] = __ldcg(xps + (m - IL) * rs);
+      ipi[m] = __ldcg(xpi + (m - IL) * rs);
     }
   } else {
 #pragma unroll
@@ -472,8 +609,8 @@ stage_kernel(const StageArgs a) {
         ips[m] = cubic(ips[m - 1], ips[m - 2], ips[m - 3], ips[m - 4]);
         ipi[m] = cubic(ipi[m - 1], ipi[m - 2], ipi[m - 3], ipi[m - 4]);
       } else {
-        ips[m] = ld2(xps + r * rs);
-        ipi[m] = ld2(xpi + r * rs);
+        ips[m] = __ldcg(xps + r * rs);
+        ipi[m] = __ldcg(xpi + r * rs);
       }
     }
   }
@@ -683,9 +820,14 @@ stage_kernel(const StageArgs a) {
     }
     if (++slot == S) { slot = 0; parity ^= 1u; }
   }
+  if ((a.px.on_lo && jb == 0) | (a.px.on_hi && je == n))
+    peer_push_halos(a.o, a.px.o_lo, a.px.o_hi, a.px.sig_lo, a.px.sig_hi, a.nchunks, n, nt,
+                    a.px.h, chunk, a.px.on_lo && jb == 0, a.px.on_hi && je == n);
   if (CHECK && __any_sync(kFull, bad) && lane == 0) {
     atomicExch(a.flag + 1, a.step >= 0 ? (unsigned long long)a.step : a.flag[2]);
-    atomicOr(a.flag, 1ull);
+    // published by the launch's last warp (tick) so no block of this launch
+    // sees a half-frozen state
+    atomicOr(a.flag + (a.tick != nullptr ? 3 : 0), 1ull);
   }
 }
 

@@ -133,6 +133,15 @@ struct hwg_solver {
   double* obs_w = nullptr;   // 32 horizon weights + ntheta projection weights
   double* obs_dev = nullptr; // 14 outputs
   double* obs_host = nullptr;
+  // fused halo push (hwg_set_peers)
+  struct Peer {
+    bool on = false;
+    double2* reg[5] = {};
+    unsigned long long* flag = nullptr;
+    long long n = 0;
+    std::vector<void*> opened;  // IPC mappings to close
+  } plo, phi;
+  long long peer_timeout_ns = 10000000000LL;
   std::string err;
 };
 
@@ -431,6 +440,9 @@ Plan make_plan(const hwg_solver* s, int stepper, int stage, DD dt) {
   return p;
 }
 
+// rows a neighbour reads across the slab edge (slabs.py HALO_ROWS)
+int halo_rows(int scheme) { return scheme == HWG_WENO5 ? 3 : scheme == HWG_WENO3 ? 2 : 4; }
+
 // step >= 0: the kernel records step + 1 on blow-up; step < 0: counter mode
 // (flag[2] is bumped by stage 0 and recorded by the scan) for graph replay
 int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, long long step) {
@@ -455,6 +467,25 @@ int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, 
     a.x = r0(p.x); a.o = r0(p.out); a.ua = r0(p.ua); a.ub = r0(p.ub); a.ug = r0(p.ug);
     a.f = r0(p.f);
     a.ca = p.ca.hi; a.cb = p.cb.hi; a.cc = p.cc.hi; a.cg = p.cg.hi; a.cd = p.cd.hi; a.ce = p.ce.hi;
+    const bool check = p.epi == EPI_RK3C || p.epi == EPI_RK104_10;
+    if (s->plo.on || s->phi.on) {
+      PeerArgs& x = a.px;
+      x.h = halo_rows(s->d.scheme);
+      x.wait = s->flag + 6;
+      x.epoch = s->flag + 5;
+      x.timeout_ns = s->peer_timeout_ns;
+      if (s->plo.on) {
+        x.on_lo = 1;
+        x.o_lo = s->plo.reg[p.out] + (size_t)(kHalo + s->plo.n) * s->rs;
+        x.sig_lo = s->plo.flag + 7;
+      }
+      if (s->phi.on) {
+        x.on_hi = 1;
+        x.o_hi = s->phi.reg[p.out] + (size_t)(kHalo - x.h) * s->rs;
+        x.sig_hi = s->phi.flag + 6;
+      }
+    }
+    if (check || s->plo.on || s->phi.on) a.tick = s->flag + 4;
     rc = launch(s, a, p.epi);
   }
   if (p.rot == 1) std::swap(s->cur, s->scr1);
@@ -719,8 +750,10 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   CK(cudaMalloc(&s->coef, CB * sizeof(double2)));
   CK(cudaMemsetAsync(s->coef, 0, CB * sizeof(double2), s->stream));
   CK(cudaMalloc(&s->cot, 2 * s->ntp * sizeof(double)));
-  CK(cudaMalloc(&s->flag, 3 * sizeof(unsigned long long)));  // blown, blowup step, step counter
-  CK(cudaMemsetAsync(s->flag, 0, 3 * sizeof(unsigned long long), s->stream));
+  // [0] blown (bit 1: peer timeout) [1] blowup step [2] step counter [3] pending
+  // blow-up [4] launch ticket [5] peer epoch [6] / [7] arrivals from lower / upper
+  CK(cudaMalloc(&s->flag, 8 * sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(s->flag, 0, 8 * sizeof(unsigned long long), s->stream));
   CK(cudaMallocHost(&s->hflag, 2 * sizeof(unsigned long long)));
   CK(cudaMallocHost(&s->obs_host, 16 * sizeof(double)));
   CK(cudaMalloc(&s->obs_dev, 16 * sizeof(double)));
@@ -823,6 +856,8 @@ void hwg_destroy(hwg_solver* s) {
   cudaSetDevice(s->dev);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (auto& e : s->graphs) cudaGraphExecDestroy(e.exec);
+  for (auto* p : {&s->plo, &s->phi})
+    for (void* m : p->opened) cudaIpcCloseMemHandle(m);
   for (int i = 0; i < s->nreg; ++i) cudaFree(s->reg[i]);
   cudaFree(s->coef);
   cudaFree(s->kdev);
@@ -835,6 +870,98 @@ void hwg_destroy(hwg_solver* s) {
   if (s->obs_host) cudaFreeHost(s->obs_host);
   if (s->own) cudaStreamDestroy(s->own);
   delete s;
+}
+
+int hwg_peer_export(hwg_solver* s, hwg_peer_desc* out) {
+  cudaSetDevice(s->dev);
+  std::memset(out, 0, sizeof(*out));
+  int rc = ensure_regs(s, 5);
+  if (rc) return rc;
+  for (int i = 0; i < 5; ++i) {
+    out->reg[i] = s->reg[i];
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, s->reg[i]));
+    std::memcpy(out->ipc[i], &h, sizeof(h));
+  }
+  out->flag = s->flag;
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, s->flag));
+  std::memcpy(out->ipc[5], &h, sizeof(h));
+  out->nrho = s->n;
+  out->row_elems = (long long)s->rs;
+  out->device = s->dev;
+  CK(cudaStreamSynchronize(s->stream));  // registers zeroed before anyone maps them
+  return HWG_OK;
+}
+
+int hwg_set_peers(hwg_solver* s, const hwg_peer_desc* lower, const hwg_peer_desc* upper,
+                  int use_ipc, double timeout_s) {
+  cudaSetDevice(s->dev);
+  if (s->ddm) {
+    s->err = "hwg_set_peers: fused halo push is implemented for the fp64 / mixed tiers";
+    return HWG_EINVAL;
+  }
+  if ((lower && s->phys_lo) || (upper && s->phys_hi)) {
+    s->err = "hwg_set_peers: a neighbour on a physical (excision / scri) end";
+    return HWG_EINVAL;
+  }
+  int rc = ensure_regs(s, 5);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(s->stream));
+  for (auto* p : {&s->plo, &s->phi}) {
+    for (void* m : p->opened) cudaIpcCloseMemHandle(m);
+    *p = hwg_solver::Peer{};
+  }
+  const hwg_peer_desc* ds[2] = {lower, upper};
+  hwg_solver::Peer* ps[2] = {&s->plo, &s->phi};
+  for (int q = 0; q < 2; ++q) {
+    const hwg_peer_desc* d = ds[q];
+    if (!d) continue;
+    if (d->row_elems != (long long)s->rs) {
+      s->err = "hwg_set_peers: neighbour row pitch differs (ntheta must match)";
+      return HWG_EINVAL;
+    }
+    hwg_solver::Peer& p = *ps[q];
+    for (int i = 0; i < 6; ++i) {
+      void* ptr = i < 5 ? d->reg[i] : d->flag;
+      if (use_ipc) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, d->ipc[i], sizeof(h));
+        CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        p.opened.push_back(ptr);
+      } else if (d->device != s->dev) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(d->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CK(e);
+      }
+      if (i < 5) p.reg[i] = static_cast<double2*>(ptr);
+      else p.flag = static_cast<unsigned long long*>(ptr);
+    }
+    p.n = d->nrho;
+    p.on = true;
+  }
+  s->peer_timeout_ns = (long long)(timeout_s > 0 ? timeout_s * 1e9 : 10e9);
+  // counters, epoch and ticket restart at 0; graphs baked the old peer args
+  for (auto& e : s->graphs) cudaGraphExecDestroy(e.exec);
+  s->graphs.clear();
+  CK(cudaMemsetAsync(s->flag + 4, 0, 4 * sizeof(unsigned long long), s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return HWG_OK;
+}
+
+int hwg_peer_prime(hwg_solver* s) {
+  cudaSetDevice(s->dev);
+  const int h = halo_rows(s->d.scheme);
+  const size_t bytes = (size_t)h * s->rs * sizeof(double2);
+  const int c = s->cur;
+  if (s->plo.on)
+    CK(cudaMemcpyAsync(s->plo.reg[c] + (size_t)(kHalo + s->plo.n) * s->rs, row0(s, c), bytes,
+                       cudaMemcpyDefault, s->stream));
+  if (s->phi.on)
+    CK(cudaMemcpyAsync(s->phi.reg[c] + (size_t)(kHalo - h) * s->rs, row0(s, c) + (size_t)(s->n - h) * s->rs,
+                       bytes, cudaMemcpyDefault, s->stream));
+  CK(cudaStreamSynchronize(s->stream));
+  return HWG_OK;
 }
 
 int hwg_set_stream(hwg_solver* s, void* stream, int own) {
@@ -916,7 +1043,14 @@ int hwg_status(hwg_solver* s, int* blew, long long* step, int clear) {
   CK(cudaStreamSynchronize(s->stream));
   *blew = s->hflag[0] != 0;
   *step = *blew ? (long long)s->hflag[1] : -1;
-  if (clear) CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
+  if (clear) {
+    CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
+    CK(cudaMemsetAsync(s->flag + 3, 0, sizeof(unsigned long long), s->stream));
+  }
+  if (s->hflag[0] & 2ull) {
+    s->err = "peer halo wait timed out (a neighbour slab did not run the same stage)";
+    return HWG_ERUNTIME;
+  }
   return HWG_OK;
 }
 

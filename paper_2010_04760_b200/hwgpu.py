@@ -84,11 +84,24 @@ _lib.hwg_status.argtypes = [_vp, C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.
 _lib.hwg_launch_info.argtypes = [_vp] + [C.POINTER(C.c_int)] * 5
 _lib.hwg_synchronize.argtypes = [_vp]
 
+
+class HwgPeerDesc(C.Structure):
+    """hwg_peer_desc (include/hweno_gpu.h)."""
+    _fields_ = [("reg", _vp * 5), ("flag", _vp), ("nrho", C.c_longlong),
+                ("row_elems", C.c_longlong), ("device", C.c_int), ("ipc", (C.c_ubyte * 64) * 6)]
+
+
+_lib.hwg_peer_export.argtypes = [_vp, C.POINTER(HwgPeerDesc)]
+_lib.hwg_set_peers.argtypes = [_vp, C.POINTER(HwgPeerDesc), C.POINTER(HwgPeerDesc), C.c_int,
+                               C.c_double]
+_lib.hwg_peer_prime.argtypes = [_vp]
+
 EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg_set_stream", "hwg_set_state_dd",
             "hwg_get_state_dd", "hwg_set_state", "hwg_get_state", "hwg_rhs", "hwg_rhs_dd",
             "hwg_advance", "hwg_set_observers", "hwg_observe", "hwg_launch_stage",
             "hwg_launch_steps", "hwg_stage_input", "hwg_register_ptr",
-            "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize"]
+            "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize",
+            "hwg_peer_export", "hwg_set_peers", "hwg_peer_prime"]
 
 
 class HwgError(RuntimeError):
@@ -308,6 +321,25 @@ class GpuEvolution:
 
     def synchronize(self):
         self._chk(_lib.hwg_synchronize(self.h))
+
+    # ------------------------------------------------------- fused halo push
+    def peer_export(self) -> bytes:
+        """This slab's hwg_peer_desc (pointers + IPC handles) as bytes, to hand
+        to the neighbours (in-process or over torch.distributed)."""
+        d = HwgPeerDesc()
+        self._chk(_lib.hwg_peer_export(self.h, C.byref(d)))
+        return bytes(d)
+
+    def set_peers(self, lower: bytes | None, upper: bytes | None, ipc: bool = False,
+                  timeout_s: float = 10.0):
+        """Connect the neighbour slabs: every later stage kernel pushes its
+        boundary rows into their halos over peer memory (hwg_set_peers)."""
+        def desc(b):
+            return C.byref(HwgPeerDesc.from_buffer_copy(b)) if b is not None else None
+        self._chk(_lib.hwg_set_peers(self.h, desc(lower), desc(upper), int(ipc), timeout_s))
+
+    def peer_prime(self):
+        self._chk(_lib.hwg_peer_prime(self.h))
 
 
 def stage_bytes(stepper: str, mode: str = "mixed") -> float:

@@ -10,8 +10,16 @@ same instruction sequence wherever it sits, so the result is bitwise the
 single-GPU one.
 
 Transports:
+  * PeerSlab   — the B200 path: no per-stage collective at all.  Every stage
+                 kernel stores its boundary rows straight into the
+                 neighbours' halo rows over NVLink (CUDA IPC mappings) and
+                 bumps their arrival counters; the next stage's boundary
+                 warps wait on them (hwg_set_peers).  One process per GPU.
+  * LocalPeerSlabs — the same kernels with several slabs in one process
+                 (same-device pointers; on one GPU the slabs' stages are
+                 launched in order, so every wait is already satisfied);
   * DistSlab   — torch.distributed point-to-point (NCCL over NVLink on GPUs,
-                 gloo on CPU), one process per GPU;
+                 gloo on CPU), one process per GPU: the collective baseline;
   * LocalSlabs — several handles in one process, halos copied with
                  stream-ordered device copies (bit-identity checks on one GPU).
 """
@@ -72,6 +80,81 @@ class DistSlab:
         for st in range(ns):
             self.exchange(self.b.stage_input(stepper, st))
             self.b.launch_stage(stepper, st, dt, step)
+
+    def steps(self, stepper: str, dt, step_begin: int, nsteps: int):
+        for q in range(nsteps):
+            self.step(stepper, dt, step_begin + q)
+
+
+class PeerSlab:
+    """One rank's slab with the fused halo push (hwg_set_peers over CUDA IPC).
+    Setup is collective over `group` (descriptor all-gather + barriers); the
+    stage loop itself issues no collective."""
+
+    def __init__(self, backend, rank: int, world: int, scheme: str = "weno5", group=None,
+                 timeout_s: float = 10.0):
+        import torch.distributed as dist
+        self.b = backend
+        self.rank, self.world = rank, world
+        self.group = group
+        mine = backend.peer_export()
+        descs = [None] * world
+        dist.all_gather_object(descs, mine, group=group)
+        lower = descs[rank - 1] if rank > 0 else None
+        upper = descs[rank + 1] if rank < world - 1 else None
+        self.error = None
+        try:
+            backend.set_peers(lower, upper, ipc=True, timeout_s=timeout_s)
+        except Exception as e:  # e.g. CUDA IPC not permitted: every rank still reaches the barrier
+            self.error = e
+        dist.barrier(group=group)
+
+    def prime(self):
+        """Initial halos of the current register (after set_state on every rank)."""
+        import torch.distributed as dist
+        dist.barrier(group=self.group)
+        self.b.peer_prime()
+        dist.barrier(group=self.group)
+
+    def exchange(self, reg: int):  # the kernels carry the halos
+        return
+
+    def step(self, stepper: str, dt, step: int):
+        ns = 3 if stepper == "ssprk33" else 10
+        for st in range(ns):
+            self.b.launch_stage(stepper, st, dt, step)
+
+    def steps(self, stepper: str, dt, step_begin: int, nsteps: int):
+        self.b.launch_steps(stepper, dt, step_begin, nsteps)
+
+
+class LocalPeerSlabs:
+    """Fused-halo slabs in one process on ONE device: all slabs launch on one
+    stream, slab by slab and stage by stage, so a stage kernel only ever waits
+    for kernels that already finished (never for a concurrently running one)."""
+
+    def __init__(self, backends, timeout_s: float = 10.0):
+        import torch
+        self.bs = list(backends)
+        self.stream = torch.cuda.Stream()
+        for b in self.bs:
+            b.set_stream(self.stream.cuda_stream)
+        d = [b.peer_export() for b in self.bs]
+        for i, b in enumerate(self.bs):
+            b.set_peers(d[i - 1] if i > 0 else None, d[i + 1] if i + 1 < len(d) else None,
+                        ipc=False, timeout_s=timeout_s)
+
+    def prime(self):
+        for b in self.bs:
+            b.synchronize()
+        for b in self.bs:
+            b.peer_prime()
+
+    def step(self, stepper: str, dt, step: int):
+        ns = 3 if stepper == "ssprk33" else 10
+        for st in range(ns):
+            for b in self.bs:
+                b.launch_stage(stepper, st, dt, step)
 
     def steps(self, stepper: str, dt, step_begin: int, nsteps: int):
         for q in range(nsteps):

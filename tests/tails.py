@@ -48,6 +48,20 @@ def window_rel_drift(t, z, t0, t1):
     return float((a.max() - a.min()) / abs(a.mean()))
 
 
+def window_mean_abs_shift(t, v, shift, t0, t1):
+    """artifacts::window_mean_abs_shift (proj/tests/support/artifacts.hpp:95-107):
+    mean |v + shift| over the window; None where the reference throws (empty)."""
+    m = (t >= t0) & (t <= t1)
+    return float(np.mean(np.abs(v[m] + shift))) if m.any() else None
+
+
+def p_phi_deviation(rows, window):
+    """criterion 8's per-scheme figure (acceptance_tails.cpp:45-48): window mean
+    of |p(Phi) + 1|."""
+    tp, pp = local_power_index(*series(rows, "phi"))
+    return window_mean_abs_shift(tp, pp, 1.0, *window)
+
+
 def summary(rows, window):
     t0, t1 = window
     tau, phi = series(rows, "phi")

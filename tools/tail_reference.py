@@ -21,6 +21,17 @@ RUNS = {
     "weno5_mixed": dict(phys=Physics(a=1.0, spin=-2, mmode=0, ell=2, center=1.0, width=0.22),
                         nrho=2048, ntheta=32, scheme="weno5", mode="mixed", stepper="ssprk104",
                         tau_end=500.0, window=(400.0, 500.0)),
+    # criterion 8's comparison runs (tail_weno3_mixed.ini, tail_fd6ko_mixed.ini,
+    # fd6ko_nodiss.ini): same physics/grid, other scheme / sigma
+    "weno3_mixed": dict(phys=Physics(a=1.0, spin=-2, mmode=0, ell=2, center=1.0, width=0.22),
+                        nrho=2048, ntheta=32, scheme="weno3", mode="mixed", stepper="ssprk104",
+                        tau_end=500.0, window=(400.0, 500.0)),
+    "fd6ko_mixed": dict(phys=Physics(a=1.0, spin=-2, mmode=0, ell=2, center=1.0, width=0.22),
+                        nrho=2048, ntheta=32, scheme="fd6ko", mode="mixed", stepper="ssprk104",
+                        tau_end=500.0, window=(400.0, 500.0), sigma=0.01),
+    "fd6ko_nodiss": dict(phys=Physics(a=1.0, spin=-2, mmode=0, ell=2, center=1.0, width=0.22),
+                         nrho=2048, ntheta=32, scheme="fd6ko", mode="mixed", stepper="ssprk104",
+                         tau_end=200.0, window=(150.0, 200.0), sigma=0.0),
     "price_schw": dict(phys=Physics(a=0.0, spin=0, mmode=0, ell=2, center=3.0, width=0.3),
                        nrho=1024, ntheta=16, scheme="weno5", mode="mixed", stepper="ssprk104",
                        tau_end=800.0, window=(500.0, 750.0)),
@@ -31,13 +42,14 @@ def run(name):
     c = RUNS[name]
     workers = os.cpu_count() or 8
     ref = RefSolver(c["phys"], c["nrho"], c["ntheta"], scheme=c["scheme"], mode=c["mode"],
-                    workers=workers)
+                    sigma=c.get("sigma", 0.01), workers=workers)
     t0 = time.time()
     rows, st = ref.run_series(c["phys"], c["stepper"], tau_end=c["tau_end"])
     print(name, st, f"{time.time() - t0:.0f}s", flush=True)
     np.savez_compressed(os.path.join(ROOT, "tests", "golden", f"tail_{name}.npz"), rows=rows,
                         window=np.array(c["window"]), steps=st["steps_done"],
-                        planned=st["planned"], wall=st["wall_seconds"], workers=workers)
+                        planned=st["planned"], wall=st["wall_seconds"], workers=workers,
+                        blew_up=st["blew_up"], blowup_step=st["blowup_step"])
 
 
 if __name__ == "__main__":
