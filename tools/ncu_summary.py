@@ -78,7 +78,8 @@ def main():
         lines += ["", f"mean DRAM bytes per launch: {mean:.4e}"]
         open(os.path.join(ROOT, "profiles", f"{tag}_ncu_{name}.md"), "w").write(
             "\n".join(lines) + "\n")
-        mode = "mixed" if "mixed" in name else "f64"
+        # report names end in the tier: ..._mixed, ..._f64, ..._ddmixed, ..._ddfull
+        mode = name.rsplit("_", 1)[-1]
         traffic[f"{mode}_65536x512"] = mean
         print(name, mean)
     json.dump(traffic, open(tfile, "w"), indent=1)
