@@ -41,6 +41,9 @@
 #ifndef HWG_MINB
 #define HWG_MINB 4  // resident blocks per SM (16 warps): caps registers at 128
 #endif
+#ifndef HWG_MINB_F64
+#define HWG_MINB_F64 3  // fp64 weights: 12 warps at up to 168 registers (measured faster)
+#endif
 #ifndef HWG_RING
 #define HWG_RING 3  // bulk-copy ring depth per warp
 #endif
@@ -201,6 +204,16 @@ __device__ __forceinline__ double weno5_lin(double f0, double f1, double f2, dou
 }
 
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+
+// 1 / s for a sum s = 1 + d of promoted fp32 weights that were normalised in
+// fp32 (|d| <= a few fp32 ulps, ~1e-6): 1 - d + d^2 is exact to ~d^3 < 1e-18,
+// below fp64 rounding, in two dependent FP64 ops instead of a reciprocal
+// (the reference's renormalisation in work precision, spatial.hpp:84-90).
+// s - 1 is exact (Sterbenz); a NaN sum stays NaN.
+__device__ __forceinline__ double renorm_inv(double s) {
+  const double d = s - 1.0;
+  return fma(d, d, 1.0 - d);
+}
 __device__ __forceinline__ float2 dem2(double2 v) { return make_float2((float)v.x, (float)v.y); }
 
 // MIXED (the paper's mode): window demoted to fp32, smoothness indicators
@@ -234,14 +247,14 @@ __device__ __forceinline__ double2 weno5_mixed2(double2 f0, double2 f1, double2 
     double c0 = fma(11.0, f2_.x, fma(-7.0, f1.x, 2.0 * f0.x));
     double c1 = fma(2.0, f3.x, fma(5.0, f2_.x, -f1.x));
     double c2 = fma(5.0, f3.x, fma(2.0, f2_.x, -f4.x));
-    out.x = fma(W2, c2, fma(W1, c1, W0 * c0)) * drcp((W0 + W1) + W2);
+    out.x = fma(W2, c2, fma(W1, c1, W0 * c0)) * renorm_inv((W0 + W1) + W2);
   }
   {
     const double W0 = w0.y, W1 = w1.y, W2 = w2.y;
     double c0 = fma(11.0, f2_.y, fma(-7.0, f1.y, 2.0 * f0.y));
     double c1 = fma(2.0, f3.y, fma(5.0, f2_.y, -f1.y));
     double c2 = fma(5.0, f3.y, fma(2.0, f2_.y, -f4.y));
-    out.y = fma(W2, c2, fma(W1, c1, W0 * c0)) * drcp((W0 + W1) + W2);
+    out.y = fma(W2, c2, fma(W1, c1, W0 * c0)) * renorm_inv((W0 + W1) + W2);
   }
   return out;
 }
@@ -269,9 +282,9 @@ __device__ __forceinline__ double2 weno3_mixed2(double2 f0, double2 f1, double2 
   const float2 x0 = __fmul2_rn(a0, inv), x1 = __fmul2_rn(a1, inv);
   double2 out;
   out.x = fma((double)x1.x, f1.x + f2_.x, (double)x0.x * fma(3.0, f1.x, -f0.x)) *
-          drcp((double)x0.x + (double)x1.x);
+          renorm_inv((double)x0.x + (double)x1.x);
   out.y = fma((double)x1.y, f1.y + f2_.y, (double)x0.y * fma(3.0, f1.y, -f0.y)) *
-          drcp((double)x0.y + (double)x1.y);
+          renorm_inv((double)x0.y + (double)x1.y);
   return out;
 }
 
@@ -311,11 +324,7 @@ template <int SCH>
 struct Win {
   // register windows, rows j - L .. j + R (L + R >= 4 so the cubic scri
   // continuation always has its four predecessors in registers)
-#ifdef HWG_UNROLL
-  static constexpr int SL = (SCH == FD6KO) ? 4 : 2;  // Psi (same width as pi: one period)
-#else
   static constexpr int SL = (SCH == FD6KO) ? 4 : (SCH == WENO5 ? 1 : 2);  // Psi
-#endif
   static constexpr int PL = (SCH == FD6KO) ? 4 : 2;                       // pi
   static constexpr int R = (SCH == FD6KO) ? 4 : (SCH == WENO5 ? 3 : 2);
   static constexpr int SW = SL + R + 1, PW = PL + R + 1;
@@ -365,13 +374,15 @@ struct Slot {
   static constexpr int S = HAS_BG ? 2 : HWG_RING;      // ring depth
 };
 
+// shared memory per block: the warps' rings, their mbarriers, then (16-byte
+// aligned) per warp the theta-extended Psi row (36 double2) of the theta operator
+template <int EPI>
+__host__ __device__ constexpr size_t stage_theta_offset(int wpb) {
+  return ((size_t)wpb * Slot<EPI>::S * (Slot<EPI>::BYTES + 8) + 15) & ~(size_t)15;
+}
 template <int EPI>
 constexpr size_t stage_smem_bytes(int wpb = kWarpsPerBlock) {
-#ifdef HWG_SMEM_THETA
-  return (size_t)wpb * Slot<EPI>::S * (Slot<EPI>::BYTES + 8) + (size_t)wpb * 36 * 16;
-#else
-  return (size_t)wpb * Slot<EPI>::S * (Slot<EPI>::BYTES + 8);
-#endif
+  return stage_theta_offset<EPI>(wpb) + (size_t)wpb * 36 * 16;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -496,7 +507,7 @@ template <int SCH, int MODE, int EPI>
 __device__ __forceinline__ void stage_body(const StageArgs& a);
 
 template <int SCH, int MODE, int EPI>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_MINB)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MODE == F64 ? HWG_MINB_F64 : HWG_MINB)
 stage_kernel(const StageArgs a) {
   if (a.flag != nullptr && *(volatile unsigned long long*)a.flag != 0ull) {  // frozen
     // a frozen slab still releases its neighbours for this stage (no data)
@@ -635,10 +646,6 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
   double2 hn = has_h ? ld2(hrow) : make_double2(0.0, 0.0);
   int slot = 0;
   uint32_t parity = 0;
-#ifdef HWG_UNROLL
-  constexpr int kUnroll = HWG_UNROLL;
-#pragma unroll kUnroll
-#endif
   for (int j = jb; j < je; ++j) {
     const unsigned char* sl = ring + (size_t)slot * SB;
     const double2* sd = reinterpret_cast<const double2*>(sl) + lane;
@@ -701,23 +708,14 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
         img = ld2(a.x + (ptrdiff_t)j * rs + psi_off(k0 + wsrc));
       if (!active) wv = wflip ? neg2(img) : img;
     }
-#ifdef HWG_SMEM_THETA
     // the chunk's extended row E[i] = Psi(k0 - 2 + i), i < 36, in shared memory
-    double2* trow = reinterpret_cast<double2*>(smem + (size_t)wpb * S * (SB + 8)) + wib * 36;
+    // (one store + four loads instead of 12 double shuffles and selects)
+    double2* trow = reinterpret_cast<double2*>(smem + stage_theta_offset<EPI>(wpb)) + wib * 36;
     trow[lane + 2] = wv;
     if (lane < 2) trow[lane] = h;
     else if (lane >= 30) trow[lane + 4] = h;
     __syncwarp();
     const double2 m2 = trow[lane], m1 = trow[lane + 1], p1 = trow[lane + 3], p2 = trow[lane + 4];
-#else
-    const double2 su2 = shfl_up2(wv, 2), su1 = shfl_up2(wv, 1);
-    const double2 sd1 = shfl_dn2(wv, 1), sd2 = shfl_dn2(wv, 2);
-    const double2 hd1 = shfl_dn2(h, 1), hu1 = shfl_up2(h, 1);
-    const double2 m2 = lane >= 2 ? su2 : h;
-    const double2 m1 = lane >= 1 ? su1 : hd1;
-    const double2 p1 = lane <= 30 ? sd1 : hu1;
-    const double2 p2 = lane <= 29 ? sd2 : h;
-#endif
     const double d1R = fma(8.0, p1.x - m1.x, m2.x - p2.x) * a.inv1;
     const double d1I = fma(8.0, p1.y - m1.y, m2.y - p2.y) * a.inv1;
     const double d2R = fma(-30.0, ps.x, fma(16.0, m1.x + p1.x, -(m2.x + p2.x))) * a.inv2;

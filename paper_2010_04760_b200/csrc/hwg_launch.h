@@ -10,7 +10,9 @@ namespace hwg {
 // fp64 / mixed / linear tiers (stage_kernel)
 void launch_stage_fast(const StageArgs& a, int scheme, int mode, int epi, int blocks, int wpb,
                        cudaStream_t stream);
-cudaError_t occupancy_fast(int* blocks_per_sm);   // also sets every kernel's smem attribute
+// resident blocks per SM of the tier's kernels (they differ by mode); also
+// sets every kernel's smem attribute
+cudaError_t occupancy_fast(int* blocks_per_sm, int mode);
 void init_attributes_fast();
 // double-double tiers (stage_kernel_dd)
 void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks, int wpb,

@@ -806,7 +806,7 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   {
     int nsm = 148, occ = 1;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->dev));
-    CK(ddm ? occupancy_dd(&occ) : occupancy_fast(&occ));
+    CK(ddm ? occupancy_dd(&occ) : occupancy_fast(&occ, mode_of(s)));
     const long long target = (long long)nsm * std::max(occ, 1) * kWarpsPerBlock;
     long long nr = std::max<long long>(1, target / s->nchunks);
     int minrows = 4;  // rows per range (the window warm-up costs ~2 rows of work)

@@ -29,14 +29,20 @@ void init_attributes_fast() {
   (void)done;
 }
 
-cudaError_t occupancy_fast(int* occ) {
-  init_attributes_fast();
-  cudaError_t e = cudaFuncSetAttribute(stage_kernel<WENO5, F64, EPI_RK3>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)stage_smem_bytes<EPI_RK3>());
+template <int MODE>
+static cudaError_t occupancy_mode(int* occ) {
+  const size_t sm = stage_smem_bytes<EPI_RK3>();
+  cudaError_t e = cudaFuncSetAttribute(stage_kernel<WENO5, MODE, EPI_RK3>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, stage_kernel<WENO5, F64, EPI_RK3>,
-                                                       kWarpsPerBlock * 32,
-                                                       stage_smem_bytes<EPI_RK3>());
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, stage_kernel<WENO5, MODE, EPI_RK3>,
+                                                       kWarpsPerBlock * 32, sm);
+}
+
+cudaError_t occupancy_fast(int* occ, int mode) {
+  init_attributes_fast();
+  if (mode == F64) return occupancy_mode<F64>(occ);
+  if (mode == MIXED) return occupancy_mode<MIXED>(occ);
+  return occupancy_mode<LIN>(occ);
 }
 }  // namespace hwg
