@@ -20,6 +20,7 @@ One JSON line on rank 0.  See DESIGN.md §5 for the roofline bookkeeping.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -98,8 +99,10 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4)
                           if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        pw = [float(r[2]) for r in rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "power_w_median": float(np.median(pw)) if pw else None,
                 "samples": len(rows)}
 
 
@@ -369,6 +372,45 @@ def e2e_mode(g, args, prob, world, rank, torch, dist, dt, runner=None):
                                      get_state=1e3 * tot[2], wall_per_step=1e3 * wall / ke))
 
 
+def e2e_advance_mode(g, args, prob, dt, torch):
+    """The drop-in's own usage of the boundary (the reference's driver calls
+    advance_steps once per run, driver.cpp:93): one hwg_advance call over K
+    steps with the HOST state in and out (pinned FieldLayout, hwg_set_state /
+    hwg_get_state inside the timed region) and the observers read back to the
+    host at every step through the hook (every = 1; the reference samples at
+    round(0.25/dt)).  Reported beside the strict per-step round trip (e2e)."""
+    from paper_2010_04760_b200 import synthetic
+    from paper_2010_04760_b200.hwgpu import HwgObservables, _lib, _p
+    nrho, nth = prob["nrho"], prob["ntheta"]
+    hw = np.zeros((4, 8))
+    hw[0, 0] = 1.0                                   # Phi(rho_min)
+    hw[1, :4] = np.array([-11.0, 18.0, -9.0, 2.0]) / (6.0 * prob["drho"])  # one-sided d/drho
+    g.set_observers(nth // 2, 0, hw, nrho // 2, np.full(nth, 1.0 / nth))
+    u = torch.empty(g.shape, dtype=torch.float64, pin_memory=True).numpy()
+    u[...] = synthetic.initial_state(prob)
+    out = torch.empty(g.shape, dtype=torch.float64, pin_memory=True).numpy()
+    K = args.steps
+    seen = []
+    hook = lambda step, tau, obs: seen.append(obs["dphi"][0])  # noqa: E731
+    g.set_state(u)
+    g.advance("ssprk33", dt, 0, 2, every=1, hook=hook)      # warm
+    g._chk(_lib.hwg_get_state(g.h, _p(out)))
+    seen.clear()
+    t0 = time.perf_counter()
+    g.set_state(u)
+    st = g.advance("ssprk33", dt, 0, K, every=1, hook=hook)
+    g._chk(_lib.hwg_get_state(g.h, _p(out)))
+    wall = time.perf_counter() - t0
+    if st["blew_up"] or st["steps_done"] != K or len(seen) != K + 1:
+        raise RuntimeError(f"e2e advance: {st}, {len(seen)} hook calls")
+    ob = ctypes.sizeof(HwgObservables)
+    return {"value": nrho * nth * 3 * K / wall, "unit": UNIT,
+            "h2d_bytes_per_step": u.nbytes / K,
+            "d2h_bytes_per_step": (out.nbytes + (K + 1) * ob) / K, "steps": K,
+            "path": "C ABI hwg_set_state + hwg_advance(K steps, observers to the host every "
+                    "step) + hwg_get_state, pinned host FieldLayout fp64"}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -413,6 +455,7 @@ def run_b200(args):
             gd.close()
             results[mode] = r
     e2e = e2e_mode(g, args, prob, world, rank, torch, dist, head["dt"], head["runner"])
+    e2e_adv = e2e_advance_mode(g, args, prob, head["dt"], torch) if world == 1 else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r, cores, sample, kind = cpu_reference_rate(args.cpu_seconds)
@@ -457,6 +500,7 @@ def run_b200(args):
                 "ms_per_step": e2e["ms"],
                 "path": "C ABI hwg_set_state + 1 RK3 step + hwg_get_state (pinned host "
                         "FieldLayout fp64); independent jobs, 'lanes' in flight"},
+        "e2e_advance": e2e_adv,
         "gpu_launches": 3 * K,
         "launch": info,
         "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / r["K"], "steps": r["K"],

@@ -99,8 +99,6 @@ struct StageArgs {
   double eps4;                     // fp64 weights: 4 eps (scaled indicators)
   double eps;                      // fp64 weno3
   float epsf;                      // fp32 weights: eps demoted
-  double iscale;                   // radial derivative scale
-  double inv1, inv2;               // theta: 1/(12 dth), 1/(12 dth^2)
   double ko;                       // KO8: sigma / (256 drho)
   double ca, cb, cc, cg, cd, ce;   // epilogue coefficients
   // state registers at row 0 (halo rows at negative offsets), blocked layout
@@ -166,7 +164,7 @@ __device__ __forceinline__ double drcp(double x) {
 // ---------------------------------------------------------------------------
 // WENO5-JS interface values (spatial.hpp:29-92) of both components of an
 // oriented window f0..f4 (double2 = real, imaginary), returned WITHOUT the
-// 1/6 factor (folded into iscale).
+// 1/6 factor (folded with 1/drho into the coefficient planes b, lam, w).
 //
 // F64: alpha_k = d_k/(eps + IS_k)^2 normalised.  With the indicators scaled
 // by 4 (IS' = 13/3 t^2 + s^2, eps' = 4 eps) the weights are
@@ -259,7 +257,7 @@ __device__ __forceinline__ double2 weno5_mixed2(double2 f0, double2 f1, double2 
   return out;
 }
 
-// WENO3 (spatial.hpp:94-130), without the 1/2 (folded into iscale)
+// WENO3 (spatial.hpp:94-130), without the 1/2 (folded into b, lam, w)
 __device__ __forceinline__ double weno3_f64(double f0, double f1, double f2, double eps) {
   double d0 = f1 - f0, d1 = f2 - f1;
   double e0 = fma(d0, d0, eps), e1 = fma(d1, d1, eps);
@@ -660,7 +658,8 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
     if (SCH != FD6KO) {
       // Psi rows: right-biased everywhere (b <= 0; evolve.cpp:103-104)
       const double2 cs = iface2_at<SCH, MODE, SL>(wps, true, 0, a);
-      dps = make_double2((cs.x - fps.x) * a.iscale, (cs.y - fps.y) * a.iscale);
+      // unscaled differences: 1/(6 drho) lives in the planes b, lam, w
+      dps = make_double2(cs.x - fps.x, cs.y - fps.y);
       fps = cs;
       // pi rows: minus where lam < 0 (split_k rule, evolve.cpp:19-30, 105-110)
       const bool o = bl.y < 0.0;
@@ -681,12 +680,12 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
       double2 pp;
       if (__all_sync(kFull, !o)) pp = iface2_at<SCH, MODE, PL>(wpi, false, 0, a);
       else pp = iface2_at<SCH, MODE, PL>(wpi, o, 0, a);
-      dpi = make_double2((pp.x - fpi.x) * a.iscale, (pp.y - fpi.y) * a.iscale);
+      dpi = make_double2(pp.x - fpi.x, pp.y - fpi.y);
       fpi = pp;
     } else {
       // FD6 (spatial.hpp:178-182): centred, no upwinding, all four rows
       auto fd6 = [&](double m3, double m2, double m1, double p1, double p2, double p3) {
-        return fma(45.0, p1 - m1, fma(-9.0, p2 - m2, p3 - m3)) * a.iscale;
+        return fma(45.0, p1 - m1, fma(-9.0, p2 - m2, p3 - m3));  // 1/(60 drho) in the planes
       };
       constexpr int C = SL;
       dps = make_double2(
@@ -716,10 +715,12 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
     else if (lane >= 30) trow[lane + 4] = h;
     __syncwarp();
     const double2 m2 = trow[lane], m1 = trow[lane + 1], p1 = trow[lane + 3], p2 = trow[lane + 4];
-    const double d1R = fma(8.0, p1.x - m1.x, m2.x - p2.x) * a.inv1;
-    const double d1I = fma(8.0, p1.y - m1.y, m2.y - p2.y) * a.inv1;
-    const double d2R = fma(-30.0, ps.x, fma(16.0, m1.x + p1.x, -(m2.x + p2.x))) * a.inv2;
-    const double d2I = fma(-30.0, ps.y, fma(16.0, m1.y + p1.y, -(m2.y + p2.y))) * a.inv2;
+    // 12 dth^2 (d_thth + cot d_th): the factor 1/(12 dth^2) is folded into
+    // ath and cot carries dth (coefficient upload, hwg_solver.cu)
+    const double d1R = fma(8.0, p1.x - m1.x, m2.x - p2.x);
+    const double d1I = fma(8.0, p1.y - m1.y, m2.y - p2.y);
+    const double d2R = fma(-30.0, ps.x, fma(16.0, m1.x + p1.x, -(m2.x + p2.x)));
+    const double d2I = fma(-30.0, ps.y, fma(16.0, m1.y + p1.y, -(m2.y + p2.y)));
     const double angR = fma(cot, d1R, d2R);
     const double angI = fma(cot, d1I, d2I);
 
@@ -748,36 +749,36 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
       f3 -= ko8(wpi[0].y, wpi[1].y, wpi[2].y, wpi[3].y, wpi[4].y, wpi[5].y, wpi[6].y, wpi[7].y, wpi[8].y);
     }
 
-    // ---- RK epilogue (timestep.hpp:61-70, 84-108), reference evaluation order
+    // ---- RK epilogue (timestep.hpp:61-70, 84-108): the reference's
+    // combinations, with its multiply-adds fused
     double2 ops, opv;
     if (EPI == EPI_RHS) {
       ops = make_double2(f0, f1); opv = make_double2(f2v, f3);
     } else if (EPI == EPI_AXPY) {
-      ops = make_double2(ps.x + a.cg * f0, ps.y + a.cg * f1);
-      opv = make_double2(pv.x + a.cg * f2v, pv.y + a.cg * f3);
+      ops = make_double2(fma(a.cg, f0, ps.x), fma(a.cg, f1, ps.y));
+      opv = make_double2(fma(a.cg, f2v, pv.x), fma(a.cg, f3, pv.y));
     } else {
       const double2* sa = reinterpret_cast<const double2*>(sl + SlotT::A) + lane;
       const double2 aps = sa[0], api = sa[32];
       if (EPI == EPI_RK3 || EPI == EPI_RK3C) {
-        ops = make_double2(a.ca * aps.x + a.cb * (ps.x + a.cg * f0),
-                           a.ca * aps.y + a.cb * (ps.y + a.cg * f1));
-        opv = make_double2(a.ca * api.x + a.cb * (pv.x + a.cg * f2v),
-                           a.ca * api.y + a.cb * (pv.y + a.cg * f3));
+        ops = make_double2(fma(a.ca, aps.x, a.cb * fma(a.cg, f0, ps.x)),
+                           fma(a.ca, aps.y, a.cb * fma(a.cg, f1, ps.y)));
+        opv = make_double2(fma(a.ca, api.x, a.cb * fma(a.cg, f2v, pv.x)),
+                           fma(a.ca, api.y, a.cb * fma(a.cg, f3, pv.y)));
       } else if (EPI == EPI_RK104_5) {
-        ops = make_double2(a.ca * aps.x + a.cb * ps.x + a.cg * f0,
-                           a.ca * aps.y + a.cb * ps.y + a.cg * f1);
-        opv = make_double2(a.ca * api.x + a.cb * pv.x + a.cg * f2v,
-                           a.ca * api.y + a.cb * pv.y + a.cg * f3);
+        ops = make_double2(fma(a.cg, f0, fma(a.cb, ps.x, a.ca * aps.x)),
+                           fma(a.cg, f1, fma(a.cb, ps.y, a.ca * aps.y)));
+        opv = make_double2(fma(a.cg, f2v, fma(a.cb, pv.x, a.ca * api.x)),
+                           fma(a.cg, f3, fma(a.cb, pv.y, a.ca * api.y)));
       } else {
         const double2* sb = reinterpret_cast<const double2*>(sl + SlotT::B) + lane;
         const double2* sg = reinterpret_cast<const double2*>(sl + SlotT::G) + lane;
         const double2 bps = sb[0], bpi = sb[32], gps = sg[0], gpi = sg[32];
-        ops = make_double2(
-            a.ca * aps.x + a.cb * bps.x + a.cc * ps.x + a.cg * (a.cd * gps.x + a.ce * f0),
-            a.ca * aps.y + a.cb * bps.y + a.cc * ps.y + a.cg * (a.cd * gps.y + a.ce * f1));
-        opv = make_double2(
-            a.ca * api.x + a.cb * bpi.x + a.cc * pv.x + a.cg * (a.cd * gpi.x + a.ce * f2v),
-            a.ca * api.y + a.cb * bpi.y + a.cc * pv.y + a.cg * (a.cd * gpi.y + a.ce * f3));
+        auto c10 = [&](double A, double B, double x, double G, double f) {
+          return fma(a.cg, fma(a.cd, G, a.ce * f), fma(a.cc, x, fma(a.cb, B, a.ca * A)));
+        };
+        ops = make_double2(c10(aps.x, bps.x, ps.x, gps.x, f0), c10(aps.y, bps.y, ps.y, gps.y, f1));
+        opv = make_double2(c10(api.x, bpi.x, pv.x, gpi.x, f2v), c10(api.y, bpi.y, pv.y, gpi.y, f3));
       }
     }
     if (active) {

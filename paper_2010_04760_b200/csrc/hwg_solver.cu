@@ -217,9 +217,9 @@ __global__ void relayout_kernel2(const double* __restrict__ src, double* __restr
 }
 
 // coefficient plane q (index j + ld*k, rows row0..) -> blocked coefficient
-// member; lo = 1 writes the DD low limbs (block offset kCoefBlk)
+// member, times `scale`; lo = 1 writes the DD low limbs (block offset kCoefBlk)
 __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, double* coef,
-                            int q, int n, int nt, int nchunks, int cblk, int lo) {
+                            int q, int n, int nt, int nchunks, int cblk, int lo, double scale) {
   __shared__ double tile[32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -235,7 +235,7 @@ __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, do
       size_t o;
       if (q < 8) o = (blk + (q / 2) * 32 + (k & 31)) * 2 + (q % 2);
       else o = (blk + kCoefAth) * 2 + (k & 31);
-      coef[o] = (k < nt) ? tile[tx][jj] : 0.0;
+      coef[o] = (k < nt) ? tile[tx][jj] * scale : 0.0;
     }
   }
 }
@@ -314,6 +314,19 @@ int launch(hwg_solver* s, const StageArgsDD& a, int epi) {
 // row-0 pointer of state register r
 double2* row0(const hwg_solver* s, int r) { return s->reg[r] + (size_t)kHalo * s->rs; }
 
+// 1/(6 drho) (WENO5), 1/(2 drho) (WENO3), 1/(60 drho) (FD6): the factor of
+// the radial differences, spatial.hpp:152, :178-182
+double radial_scale(const hwg_solver* s) {
+  const double dr = s->d.drho;
+  if (s->d.scheme == HWG_WENO5) return 1.0 / (6.0 * dr);
+  if (s->d.scheme == HWG_WENO3) return 1.0 / (2.0 * dr);
+  return 1.0 / (60.0 * dr);
+}
+// 1/(12 dth^2): the second-derivative factor of the theta operator (spatial.hpp:212)
+double theta_scale(const hwg_solver* s) {
+  return 1.0 / (12.0 * s->d.dtheta * s->d.dtheta);
+}
+
 StageArgs base_args(const hwg_solver* s) {
   StageArgs a{};
   a.n = s->n; a.nt = s->nt; a.nchunks = s->nchunks;
@@ -324,11 +337,6 @@ StageArgs base_args(const hwg_solver* s) {
   a.eps = s->d.eps;
   a.epsf = (float)s->d.eps;
   const double dr = s->d.drho;
-  if (s->d.scheme == HWG_WENO5) a.iscale = 1.0 / (6.0 * dr);
-  else if (s->d.scheme == HWG_WENO3) a.iscale = 1.0 / (2.0 * dr);
-  else a.iscale = 1.0 / (60.0 * dr);
-  a.inv1 = 1.0 / (12.0 * s->d.dtheta);
-  a.inv2 = 1.0 / (12.0 * s->d.dtheta * s->d.dtheta);
   a.ko = s->d.sigma / (256.0 * dr);
   a.coef = s->coef;
   a.cot = s->cot;
@@ -775,8 +783,12 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
         } else {
           CK(cudaMemsetAsync(tmp, 0, plane_src * sizeof(double), s->stream));
         }
+        // fast tiers: the radial derivative scale is folded into the planes
+        // that multiply radial derivatives (b, lam, w) and the theta scale
+        // 1/(12 dth^2) into ath (stage_body); the DD tiers keep the planes
+        const double sc = ddm ? 1.0 : (q < 4 ? radial_scale(s) : q == 8 ? theta_scale(s) : 1.0);
         coef_kernel<<<grid, blk, 0, s->stream>>>(tmp, ld, row0_, reinterpret_cast<double*>(s->coef),
-                                                  q, s->n, s->nt, s->nchunks, s->cblk, limb);
+                                                  q, s->n, s->nt, s->nchunks, s->cblk, limb, sc);
         CK(cudaGetLastError());
       }
     }
@@ -788,7 +800,7 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
         c[2 * k] = cotth[k];
         c[2 * k + 1] = cot_lo ? cot_lo[k] : 0.0;
       } else {
-        c[k] = cotth[k];
+        c[k] = cotth[k] * s->d.dtheta;  // cot * (1/(12 dth)) / (1/(12 dth^2))
       }
     }
     CK(cudaMemcpy(s->cot, c.data(), 2 * s->ntp * sizeof(double), cudaMemcpyHostToDevice));
