@@ -411,6 +411,51 @@ def e2e_advance_mode(g, args, prob, dt, torch):
                     "step) + hwg_get_state, pinned host FieldLayout fp64"}
 
 
+# the other BASELINE shapes (parity-test configurations; not the headline):
+# (label, nrho, ntheta, scheme, mode)
+CONFIG_SHAPES = [
+    ("C1 1024x64 weno5 f64", 1024, 64, "weno5", "f64"),
+    ("C2 4096x128 weno5 mixed", 4096, 128, "weno5", "mixed"),
+    ("C3 16384x128 weno5 mixed", 16384, 128, "weno5", "mixed"),
+    ("C3 16384x128 weno5 f64", 16384, 128, "weno5", "f64"),
+    ("C4 4096x128 fd6ko", 4096, 128, "fd6ko", "mixed"),
+]
+
+
+def config_rates(torch):
+    """Stage-updates/s of the same kernels at the other BASELINE shapes, one
+    handle each, whole SSP-RK3 steps replayed as a CUDA graph
+    (hwg_launch_steps) for ~50 ms after 5 warm-up steps.  C1-C4 fit in the
+    126 MB L2 (no flush: the point is the resident-grid rate) and are
+    launch/latency bound rather than HBM bound."""
+    from paper_2010_04760_b200 import hwgpu, synthetic
+    out = {}
+    stream = torch.cuda.current_stream()
+    for label, n, nt, sch, mode in CONFIG_SHAPES:
+        prob = synthetic.problem(n, nt)
+        g = hwgpu.GpuEvolution(n, nt, prob["drho"], prob["dtheta"], prob["parity"],
+                               prob["coef"], prob["cotth"], hwgpu.SchemeSpec(sch, mode))
+        g.set_stream(stream.cuda_stream)
+        g.set_state(synthetic.initial_state(prob))
+        dt = synthetic.select_dt(prob)
+        g.launch_steps("ssprk33", dt, 0, 5)
+        torch.cuda.synchronize()
+        K = int(min(5000, max(20, 0.05 * 2.5e10 / (3 * n * nt))))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.launch_steps("ssprk33", dt, 5, K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        blown, _ = g.status()
+        g.close()
+        if blown:
+            raise RuntimeError(f"{label}: state blew up")
+        out[label] = {"value": n * nt * 3 * K / (ms / 1e3), "ms_per_step": ms / K, "steps": K,
+                      "l2": "resident (grid < L2)" if n * nt * 168 < 100e6 else "streams"}
+    return out
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -456,6 +501,7 @@ def run_b200(args):
             results[mode] = r
     e2e = e2e_mode(g, args, prob, world, rank, torch, dist, head["dt"], head["runner"])
     e2e_adv = e2e_advance_mode(g, args, prob, head["dt"], torch) if world == 1 else None
+    shapes = config_rates(torch) if world == 1 and not args.no_configs else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r, cores, sample, kind = cpu_reference_rate(args.cpu_seconds)
@@ -501,6 +547,7 @@ def run_b200(args):
                 "path": "C ABI hwg_set_state + 1 RK3 step + hwg_get_state (pinned host "
                         "FieldLayout fp64); independent jobs, 'lanes' in flight"},
         "e2e_advance": e2e_adv,
+        "other_configs": shapes,
         "gpu_launches": 3 * K,
         "launch": info,
         "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / r["K"], "steps": r["K"],
@@ -535,6 +582,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dd", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--ref-nrho", type=int, default=1024)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
