@@ -222,16 +222,18 @@ __device__ __forceinline__ float2 dem2(double2 v) { return make_float2((float)v.
 __device__ __forceinline__ double2 weno5_mixed2(double2 f0, double2 f1, double2 f2_, double2 f3,
                                                 double2 f4, float eps) {
   const float2 g0 = dem2(f0), g1 = dem2(f1), g2 = dem2(f2_), g3 = dem2(f3), g4 = dem2(f4);
-  const float2 c1312 = f2(13.0f / 12.0f), qt = f2(0.25f), ep = f2(eps);
+  // indicators scaled by 4 (E = 4 (eps + IS) = 13/3 t^2 + s^2 + 4 eps): the
+  // weights are invariant under the common factor 16 of the alphas
+  const float2 c133 = f2(13.0f / 3.0f), ep = f2(4.0f * eps);
   float2 t = __fadd2_rn(__ffma2_rn(f2(-2.0f), g1, g0), g2);
   float2 s = __ffma2_rn(f2(3.0f), g2, __ffma2_rn(f2(-4.0f), g1, g0));
-  float2 e0 = __fadd2_rn(ep, __ffma2_rn(__fmul2_rn(c1312, t), t, __fmul2_rn(__fmul2_rn(qt, s), s)));
+  float2 e0 = __ffma2_rn(__fmul2_rn(c133, t), t, __ffma2_rn(s, s, ep));
   t = __fadd2_rn(__ffma2_rn(f2(-2.0f), g2, g1), g3);
   s = __ffma2_rn(f2(-1.0f), g3, g1);
-  float2 e1 = __fadd2_rn(ep, __ffma2_rn(__fmul2_rn(c1312, t), t, __fmul2_rn(__fmul2_rn(qt, s), s)));
+  float2 e1 = __ffma2_rn(__fmul2_rn(c133, t), t, __ffma2_rn(s, s, ep));
   t = __fadd2_rn(__ffma2_rn(f2(-2.0f), g3, g2), g4);
   s = __ffma2_rn(f2(3.0f), g2, __ffma2_rn(f2(-4.0f), g3, g4));
-  float2 e2 = __fadd2_rn(ep, __ffma2_rn(__fmul2_rn(c1312, t), t, __fmul2_rn(__fmul2_rn(qt, s), s)));
+  float2 e2 = __ffma2_rn(__fmul2_rn(c133, t), t, __ffma2_rn(s, s, ep));
   const float2 q0 = __fmul2_rn(e0, e0), q1 = __fmul2_rn(e1, e1), q2 = __fmul2_rn(e2, e2);
   const float2 a0 = __fmul2_rn(f2(0.1f), make_float2(frcp(q0.x), frcp(q0.y)));
   const float2 a1 = __fmul2_rn(f2(0.6f), make_float2(frcp(q1.x), frcp(q1.y)));
