@@ -320,7 +320,7 @@ def e2e_mode(g, args, prob, world, rank, torch, dist, dt, runner=None):
     from paper_2010_04760_b200 import hwgpu, slabs, synthetic
     u0 = synthetic.initial_state(prob)
     ke = max(1, min(args.e2e_steps, args.steps))
-    lanes = 2 if world == 1 and ke > 1 else 1
+    lanes = max(1, min(args.e2e_lanes, ke)) if world == 1 else 1
     hs = [g]
     for _ in range(lanes - 1):
         h = hwgpu.GpuEvolution(prob["nrho"], prob["ntheta"], prob["drho"], prob["dtheta"],
@@ -576,7 +576,9 @@ def main():
     ap.add_argument("--mode", default="mixed", choices=["mixed", "f64"])
     ap.add_argument("--nrho", type=int, default=65536)
     ap.add_argument("--ntheta", type=int, default=512)
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-lanes", type=int, default=4,
+                    help="independent e2e jobs in flight on one GPU (own handle + stream each)")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="N > 1 slab halos: fused push over NVLink peer memory, or NCCL P2P")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -216,6 +216,34 @@ __global__ void relayout_kernel2(const double* __restrict__ src, double* __restr
   }
 }
 
+// the reference's ghost rules (evolve.cpp:40-71) on an fp64 FieldLayout in
+// device memory, same arithmetic as fill_host_ghosts (no contraction):
+// blockIdx.y = 0: radial cubic continuation, one thread per (component, k);
+// blockIdx.y = 1: theta parity images, one thread per (component, j)
+__global__ void ghost_kernel(double* u, int n, int nt, int even) {
+  const long long W = n + 8, P = W * (nt + 4);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  auto at = [&](int c, int j, int k) -> double& { return u[c * P + (long long)(k + 2) * W + (j + 4)]; };
+  auto cub = [](double a, double b, double c, double d) { return 4.0 * a - 6.0 * b + 4.0 * c - d; };
+  if (blockIdx.y == 0) {
+    if (i >= 4 * nt) return;
+    const int c = i / nt, k = i % nt;
+    for (int t = 1; t <= 4; ++t)
+      at(c, -t, k) = cub(at(c, -t + 1, k), at(c, -t + 2, k), at(c, -t + 3, k), at(c, -t + 4, k));
+    for (int t = 1; t <= 4; ++t)
+      at(c, n - 1 + t, k) = cub(at(c, n - 2 + t, k), at(c, n - 3 + t, k), at(c, n - 4 + t, k),
+                                at(c, n - 5 + t, k));
+  } else {
+    if (i >= 4 * n) return;
+    const int c = i / n, j = i % n;
+    for (int t = 0; t < 2; ++t) {
+      const double north = at(c, j, t), south = at(c, j, nt - 1 - t);
+      at(c, j, -1 - t) = even ? north : -north;
+      at(c, j, nt + t) = even ? south : -south;
+    }
+  }
+}
+
 // coefficient plane q (index j + ld*k, rows row0..) -> blocked coefficient
 // member, times `scale`; lo = 1 writes the DD low limbs (block offset kCoefBlk)
 __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, double* coef,
@@ -572,9 +600,16 @@ int download_layout(hwg_solver* s, double* host, int stride, int reg, bool ghost
   relayout_kernel2<<<grid, blk, 0, s->stream>>>(nullptr, s->stage_dev, row0(s, reg), s->n, s->nt,
                                                  s->nchunks, stride, 1, s->sblk);
   CK(cudaGetLastError());
+  const bool dev_ghosts = ghosts && stride == 1;  // fp64 FieldLayout: ghosts on the device
+  if (dev_ghosts) {
+    const int m = 4 * std::max(s->n, s->nt);
+    ghost_kernel<<<dim3((m + 255) / 256, 2), 256, 0, s->stream>>>(s->stage_dev, s->n, s->nt,
+                                                                   s->d.parity > 0);
+    CK(cudaGetLastError());
+  }
   CK(cudaMemcpyAsync(host, s->stage_dev, cnt * sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   CK(cudaStreamSynchronize(s->stream));
-  if (ghosts) fill_host_ghosts(s, host, stride, s->ddm && stride == 2);
+  if (ghosts && !dev_ghosts) fill_host_ghosts(s, host, stride, s->ddm && stride == 2);
   return HWG_OK;
 }
 

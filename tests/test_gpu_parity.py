@@ -37,6 +37,21 @@ def test_rhs_fp64_matches_reference_and_oracle(cuda_ok, case):
 
 
 @pytest.mark.parametrize("case", golden_cases())
+def test_get_state_ghosts_match_reference_rules(cuda_ok, case):
+    """hwg_get_state fills the FieldLayout ghosts on the device; they equal the
+    reference's apply_boundaries (evolve.cpp:40-71, via the oracle) bit for
+    bit, and the interior round-trips exactly."""
+    g = load_golden(case)
+    gpu = gpu_from_golden(g, "f64")
+    orc = oracle_from_golden(g, "f64")
+    gpu.set_state(g["u0"])
+    ug = gpu.get_state()
+    assert np.array_equal(interior(ug), interior(g["u0"]))
+    uo, _ = orc.rhs(ug * 1.0)
+    assert np.array_equal(ug, uo)
+
+
+@pytest.mark.parametrize("case", golden_cases())
 def test_rhs_mixed_matches_reference_mixed(cuda_ok, case):
     g = load_golden(case)
     gpu = gpu_from_golden(g, "mixed")
