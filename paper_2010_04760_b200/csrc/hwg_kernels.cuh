@@ -91,6 +91,7 @@ struct PeerArgs {
 
 struct StageArgs {
   int n, nt, nchunks;
+  long long rs, crs;               // double2 per state / coefficient row (row pitch)
   int phys_lo, phys_hi;            // slab holds the excision / scri end
   int nranges;
   int negpar;                      // theta parity (-1)^(m+s) == -1
@@ -460,11 +461,10 @@ static __device__ __noinline__ void peer_wait_halos(unsigned long long* wait,
 // signal their arrival counters
 static __device__ __noinline__ void peer_push_halos(const double2* o, double2* o_lo,
                                                     double2* o_hi, unsigned long long* sig_lo,
-                                                    unsigned long long* sig_hi, int nchunks,
+                                                    unsigned long long* sig_hi, ptrdiff_t rs,
                                                     int n, int nt, int h, int chunk, bool lo,
                                                     bool hi) {
   const int lane = threadIdx.x & 31;
-  const ptrdiff_t rs = (ptrdiff_t)nchunks * kStateBlk;
   const ptrdiff_t c = chunk * kStateBlk + lane;
   const double2* ob = o + c;
   if ((chunk << 5) + lane < nt) {
@@ -545,8 +545,8 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
   const int k = k0 + lane;
   const int nt = a.nt, n = a.n;
   const bool active = k < nt;
-  const ptrdiff_t rs = (ptrdiff_t)a.nchunks * kStateBlk;  // state row stride (double2)
-  const ptrdiff_t crs = (ptrdiff_t)a.nchunks * kCoefBlk;  // coefficient row stride
+  const ptrdiff_t rs = (ptrdiff_t)a.rs;    // state row pitch (double2)
+  const ptrdiff_t crs = (ptrdiff_t)a.crs;  // coefficient row pitch
   // theta halo: lanes 0,1 hold columns k0-2, k0-1; lanes 30,31 hold k0+32, k0+33
   const bool has_h = lane < 2 || lane >= 30;
   bool hflip;
@@ -822,7 +822,7 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
     if (++slot == S) { slot = 0; parity ^= 1u; }
   }
   if ((a.px.on_lo && jb == 0) | (a.px.on_hi && je == n))
-    peer_push_halos(a.o, a.px.o_lo, a.px.o_hi, a.px.sig_lo, a.px.sig_hi, a.nchunks, n, nt,
+    peer_push_halos(a.o, a.px.o_lo, a.px.o_hi, a.px.sig_lo, a.px.sig_hi, rs, n, nt,
                     a.px.h, chunk, a.px.on_lo && jb == 0, a.px.on_hi && je == n);
   if (CHECK && __any_sync(kFull, bad) && lane == 0) {
     atomicExch(a.flag + 1, a.step >= 0 ? (unsigned long long)a.step : a.flag[2]);

@@ -109,7 +109,8 @@ struct hwg_solver {
   double* cot = nullptr;     // cot(theta) (fp64, or dd pairs), padded to nchunks*32
   double2* reg[5] = {};      // state registers, blocked layout incl. halo rows
   int nreg = 0;
-  size_t rs = 0;             // double2 per state row (nchunks * sblk)
+  size_t rs = 0;             // double2 per state row (nchunks * sblk + pad)
+  size_t crs = 0;            // double2 per coefficient row (nchunks * cblk + pad)
   size_t reg_elems = 0;      // double2 per register ((n + 2 kHalo) * rs)
   int cur = 0, scr1 = 1, scr2 = 2, scr3 = 3, scr4 = 4;
   unsigned long long* flag = nullptr;
@@ -161,13 +162,12 @@ namespace hwg {
 // host FieldLayout <-> device register (row 0 pointer), blocked; stride 2 =
 // DD {hi, lo} pairs on the host.  dd: the register holds lo limbs at +64.
 __global__ void relayout_kernel2(const double* __restrict__ src, double* __restrict__ dst,
-                                 double2* reg, int n, int nt, int nchunks, int stride, int dir,
+                                 double2* reg, int n, int nt, size_t rs, int stride, int dir,
                                  int sblk) {
   __shared__ double tile[4][32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const size_t W = (size_t)n + 8, Hh = (size_t)nt + 4, P = W * Hh;
-  const size_t rs = (size_t)nchunks * sblk;
   const bool dd = sblk == kStateBlkDD;
   for (int limb = 0; limb < 2; ++limb) {
     if (limb == 1 && !dd && !(dir == 1 && stride == 2)) break;
@@ -247,7 +247,8 @@ __global__ void ghost_kernel(double* u, int n, int nt, int even) {
 // coefficient plane q (index j + ld*k, rows row0..) -> blocked coefficient
 // member, times `scale`; lo = 1 writes the DD low limbs (block offset kCoefBlk)
 __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, double* coef,
-                            int q, int n, int nt, int nchunks, int cblk, int lo, double scale) {
+                            int q, int n, int nt, int nchunks, int cblk, size_t crs, int lo,
+                            double scale) {
   __shared__ double tile[32][33];
   const int j0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -259,7 +260,7 @@ __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, do
   for (int jj = ty; jj < 32; jj += 8) {
     const int j = j0 + jj, k = k0 + tx;
     if (j < n && k < nchunks * 32) {
-      const size_t blk = ((size_t)j * nchunks + (k >> 5)) * cblk + (lo ? kCoefBlk : 0);
+      const size_t blk = (size_t)j * crs + (size_t)(k >> 5) * cblk + (lo ? kCoefBlk : 0);
       size_t o;
       if (q < 8) o = (blk + (q / 2) * 32 + (k & 31)) * 2 + (q % 2);
       else o = (blk + kCoefAth) * 2 + (k & 31);
@@ -268,10 +269,9 @@ __global__ void coef_kernel(const double* __restrict__ src, int ld, int row0, do
   }
 }
 
-__global__ void observe_kernel2(const double2* reg, int nchunks, int sblk, int j0,
+__global__ void observe_kernel2(const double2* reg, size_t rs, int sblk, int j0,
                                 const double* hw, int kobs, int jobs, int jscri, const double* pw,
                                 int nt, double* out) {
-  const size_t rs = (size_t)nchunks * sblk;
   auto psi = [&](int j, int k) { return reg[j * rs + (size_t)(k >> 5) * sblk + (k & 31)]; };
   const int lane = threadIdx.x;
   if (lane == 0) {
@@ -358,6 +358,7 @@ double theta_scale(const hwg_solver* s) {
 StageArgs base_args(const hwg_solver* s) {
   StageArgs a{};
   a.n = s->n; a.nt = s->nt; a.nchunks = s->nchunks;
+  a.rs = (long long)s->rs; a.crs = (long long)s->crs;
   a.phys_lo = s->phys_lo; a.phys_hi = s->phys_hi;
   a.nranges = s->nranges;
   a.negpar = s->d.parity < 0 ? 1 : 0;
@@ -547,7 +548,7 @@ int upload_layout(hwg_solver* s, const double* host, int stride, int reg) {
   CK(cudaMemcpyAsync(s->stage_dev, host, cnt * sizeof(double), cudaMemcpyHostToDevice, s->stream));
   dim3 grid((s->n + 31) / 32, (s->nt + 31) / 32), blk(32, 8);
   relayout_kernel2<<<grid, blk, 0, s->stream>>>(s->stage_dev, nullptr, row0(s, reg), s->n, s->nt,
-                                                 s->nchunks, stride, 0, s->sblk);
+                                                 s->rs, stride, 0, s->sblk);
   CK(cudaGetLastError());
   return HWG_OK;
 }
@@ -598,7 +599,7 @@ int download_layout(hwg_solver* s, double* host, int stride, int reg, bool ghost
   CK(cudaMemsetAsync(s->stage_dev, 0, cnt * sizeof(double), s->stream));
   dim3 grid((s->n + 31) / 32, (s->nt + 31) / 32), blk(32, 8);
   relayout_kernel2<<<grid, blk, 0, s->stream>>>(nullptr, s->stage_dev, row0(s, reg), s->n, s->nt,
-                                                 s->nchunks, stride, 1, s->sblk);
+                                                 s->rs, stride, 1, s->sblk);
   CK(cudaGetLastError());
   const bool dev_ghosts = ghosts && stride == 1;  // fp64 FieldLayout: ghosts on the device
   if (dev_ghosts) {
@@ -759,7 +760,17 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   s->nchunks = s->ntp / 32;
   s->sblk = ddm ? kStateBlkDD : kStateBlk;
   s->cblk = ddm ? kCoefBlkDD : kCoefBlk;
-  s->rs = (size_t)s->nchunks * s->sblk;
+  // row pitches: the fast tiers may pad rows (HWG_STATE_PAD / HWG_COEF_PAD,
+  // in double2) to spread concurrent row accesses over the HBM channels
+  {
+    size_t sp = 0, cp = 0;
+    if (!ddm) {
+      if (const char* e = std::getenv("HWG_STATE_PAD")) sp = (size_t)std::max(0, std::atoi(e));
+      if (const char* e = std::getenv("HWG_COEF_PAD")) cp = (size_t)std::max(0, std::atoi(e));
+    }
+    s->rs = (size_t)s->nchunks * s->sblk + sp;
+    s->crs = (size_t)s->nchunks * s->cblk + cp;
+  }
   s->phys_lo = d->rho_offset == 0;
   s->phys_hi = d->rho_offset + d->nrho == nglob;
   s->dev = d->device;
@@ -789,7 +800,7 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   } while (0)
   CK(cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking));
   s->stream = s->own;
-  const size_t CB = (size_t)s->n * s->nchunks * s->cblk;
+  const size_t CB = (size_t)s->n * s->crs;
   CK(cudaMalloc(&s->coef, CB * sizeof(double2)));
   CK(cudaMemsetAsync(s->coef, 0, CB * sizeof(double2), s->stream));
   CK(cudaMalloc(&s->cot, 2 * s->ntp * sizeof(double)));
@@ -823,7 +834,8 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
         // 1/(12 dth^2) into ath (stage_body); the DD tiers keep the planes
         const double sc = ddm ? 1.0 : (q < 4 ? radial_scale(s) : q == 8 ? theta_scale(s) : 1.0);
         coef_kernel<<<grid, blk, 0, s->stream>>>(tmp, ld, row0_, reinterpret_cast<double*>(s->coef),
-                                                  q, s->n, s->nt, s->nchunks, s->cblk, limb, sc);
+                                                  q, s->n, s->nt, s->nchunks, s->cblk, s->crs, limb,
+                                                  sc);
         CK(cudaGetLastError());
       }
     }
@@ -1133,7 +1145,7 @@ int hwg_set_observers(hwg_solver* s, int kobs, int j0, const double* hw, int job
 }
 
 int hwg_observe(hwg_solver* s, hwg_observables* out) {
-  observe_kernel2<<<1, 32, 0, s->stream>>>(row0(s, s->cur), s->nchunks, s->sblk, s->j0, s->obs_w,
+  observe_kernel2<<<1, 32, 0, s->stream>>>(row0(s, s->cur), s->rs, s->sblk, s->j0, s->obs_w,
                                             s->kobs, s->jobs, s->phys_hi ? s->n - 1 : -1,
                                             s->obs_w + 32, s->nt, s->obs_dev);
   CK(cudaGetLastError());
