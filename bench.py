@@ -214,7 +214,8 @@ def make_runner(args, g, mode, rank, world, dist):
     return slabs.DistSlab(g, rank, world, "weno5"), ("nccl" if world > 1 else "none")
 
 
-def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmup=None):
+def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmup=None,
+              stepper="ssprk33"):
     from paper_2010_04760_b200 import hwgpu, slabs, synthetic
     spec = hwgpu.SchemeSpec("weno5", mode)
     K = steps or args.steps
@@ -227,11 +228,12 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
     g.set_stream(stream.cuda_stream)
     u0 = synthetic.initial_state(prob)
     g.set_state(u0)
-    dt = synthetic.select_dt(prob, "ssprk33")
+    dt = synthetic.select_dt(prob, stepper)
+    ns = 3 if stepper == "ssprk33" else 10
     runner, halo = make_runner(args, g, mode, rank, world, dist)
     P = prob["nrho"] * prob["ntheta"]
     for q in range(W):
-        runner.step("ssprk33", dt, q)
+        runner.step(stepper, dt, q)
     torch.cuda.synchronize()
     if halo == "peer":
         # all ranks agree the fused halo push works here, else fall back to NCCL
@@ -249,22 +251,22 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
             g.set_state(u0)
             runner, halo = slabs.DistSlab(g, rank, world, "weno5"), "nccl"
             for q in range(W):
-                runner.step("ssprk33", dt, q)
+                runner.step(stepper, dt, q)
             torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(3 * K)]
+           for _ in range(ns * K)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     i = 0
     for q in range(K):
-        for st in range(3):
-            runner.exchange(g.stage_input("ssprk33", st))
+        for st in range(ns):
+            runner.exchange(g.stage_input(stepper, st))
             evs[i][0].record(stream)
-            g.launch_stage("ssprk33", st, dt, W + q)
+            g.launch_stage(stepper, st, dt, W + q)
             evs[i][1].record(stream)
             i += 1
     t_end.record(stream)
@@ -274,14 +276,15 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
         t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    stage_ms = np.array([a.elapsed_time(b) for a, b in evs]).reshape(K, 3)
+    stage_ms = np.array([a.elapsed_time(b) for a, b in evs]).reshape(K, ns)
     blown, _ = g.status()
     if blown:
         raise RuntimeError(f"benchmark state blew up ({mode})")
-    value = world * P * 3 * K / (total_ms / 1000.0)
-    # algorithmic bytes per launch: stage 1 136 B/pt, 2-3 168 B/pt
-    # (fp64 state 32 B + coefficients 72 B); double-double tiers twice that
-    bytes_per_step = P * (136 + 168 + 168) * (2 if mode.startswith("dd") else 1)
+    value = world * P * ns * K / (total_ms / 1000.0)
+    # algorithmic bytes per step: RK3 stage 1 136 B/pt, stages
+    # 2-3 168 B/pt (fp64 state 32 B + coefficients 72 B); RK(10,4) 1520 B/pt;
+    # double-double tiers twice that
+    bytes_per_step = P * (472 if ns == 3 else 1520) * (2 if mode.startswith("dd") else 1)
     kern_ms = float(stage_ms.sum())
     achieved = bytes_per_step * K / (kern_ms / 1000.0) / 1e9
     return g, dict(value=value, total_ms=total_ms, stage_ms=stage_ms, achieved_gbs=achieved,
@@ -491,6 +494,11 @@ def run_b200(args):
     for m in list(handles):
         if m != args.mode:
             handles.pop(m).close()
+    # the reference's production stepper (all proj/configs/*.ini use ssprk104)
+    g4, r = time_mode(args, args.mode, prob, world, rank, dev, torch, dist,
+                      steps=max(1, args.steps // 3), stepper="ssprk104")
+    g4.close()
+    results[f"{args.mode}-ssprk104"] = r
     # the reference's own precisions (double-double tiers, bitwise equal to the
     # reference library): the paper's mixed-vs-full experiment on B200
     if not args.no_dd:
@@ -551,6 +559,7 @@ def run_b200(args):
         "gpu_launches": 3 * K,
         "launch": info,
         "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / r["K"], "steps": r["K"],
+                      "stepper": "ssprk104" if m.endswith("ssprk104") else "ssprk33",
                       "stage_kernel_gbs": r["achieved_gbs"], "frac": r["achieved_gbs"] / peak,
                       "stage_ms_mean": [float(x) for x in r["stage_ms"].mean(axis=0)]}
                   for m, r in results.items()},
