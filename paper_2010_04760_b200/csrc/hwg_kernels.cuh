@@ -117,6 +117,7 @@ struct StageArgs {
   // advances the peer epoch.  Null for launches that need neither.
   unsigned long long* tick;
   PeerArgs px;                     // fused halo push to the neighbour slabs (NVLink P2P)
+  int pdl;                         // launched with programmatic stream serialisation
 };
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
@@ -396,6 +397,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
+// expected bytes without arriving (the arrival comes with the later copies)
+__device__ __forceinline__ void mbar_expect_tx_only(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+// programmatic dependent launch: let the next stage's grid launch now; wait
+// for the previous stage's grid (and its memory) before touching its outputs
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -504,28 +519,24 @@ static __device__ __noinline__ void launch_ticket(unsigned long long* tick,
 }
 
 template <int SCH, int MODE, int EPI>
-__device__ __forceinline__ void stage_body(const StageArgs& a);
+__device__ __forceinline__ bool stage_body(const StageArgs& a);
 
 template <int SCH, int MODE, int EPI>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MODE == F64 ? HWG_MINB_F64 : HWG_MINB)
 stage_kernel(const StageArgs a) {
-  if (a.flag != nullptr && *(volatile unsigned long long*)a.flag != 0ull) {  // frozen
-    // a frozen slab still releases its neighbours for this stage (no data)
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (a.px.on_lo | a.px.on_hi)) {
-      if (a.px.on_lo) peer_signal(a.px.sig_lo, (unsigned long long)a.nchunks);
-      if (a.px.on_hi) peer_signal(a.px.sig_hi, (unsigned long long)a.nchunks);
-      *a.px.epoch += 1ull;
-    }
-    return;
-  }
-  if (a.bump && blockIdx.x == 0 && threadIdx.x == 0) a.flag[2] += 1ull;  // step counter
-  stage_body<SCH, MODE, EPI>(a);
+  if (!stage_body<SCH, MODE, EPI>(a)) return;  // frozen
+  // let the next stage's grid launch once this warp's rows are done (measured:
+  // triggering at kernel start lets the next grid's waiting blocks take SM
+  // slots early and costs 12 % at C5; triggering here gains 3-5 % on the
+  // launch-bound small grids and is neutral at C5)
+  pdl_trigger();
   if (a.tick != nullptr)
     launch_ticket(a.tick, a.flag, (a.px.on_lo | a.px.on_hi) ? a.px.epoch : nullptr);
 }
 
+// false: the state is frozen (an earlier step blew up) and nothing was done
 template <int SCH, int MODE, int EPI>
-__device__ __forceinline__ void stage_body(const StageArgs& a) {
+__device__ __forceinline__ bool stage_body(const StageArgs& a) {
   using Wn = Win<SCH>;
   using SlotT = Slot<EPI>;
   constexpr int SL = Wn::SL, PL = Wn::PL, R = Wn::R, SW = Wn::SW, PW = Wn::PW;
@@ -538,7 +549,7 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
   const int gw = blockIdx.x * wpb + wib;
   const int chunk = gw % a.nchunks;
   const int range = gw / a.nchunks;
-  if (range >= a.nranges) return;                       // whole warp (to the ticket)
+  const bool live = range < a.nranges;  // else the whole warp only takes its ticket
   const int jb = (int)((long long)range * a.n / a.nranges);
   const int je = (int)((long long)(range + 1) * a.n / a.nranges);
   const int k0 = chunk << 5;
@@ -557,24 +568,27 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
   bool wflip;
   const int wsrc = reflect_col(k, nt, wflip, a.negpar) - k0;
 
-  // boundary ranges: wait for the neighbours' halo rows of this stage
-  if ((a.px.on_lo && range == 0) | (a.px.on_hi && range == a.nranges - 1))
-    peer_wait_halos(a.px.wait, a.px.epoch, a.flag, a.nchunks, a.px.timeout_ns,
-                    range == 0 && a.px.on_lo, range == a.nranges - 1 && a.px.on_hi);
   unsigned char* ring = smem + (size_t)wib * S * SB;
   const uint32_t bar0 = smem_u32(smem + (size_t)wpb * S * SB) + wib * S * 8;
   const double2* xblk = a.x + chunk * kStateBlk;         // this chunk's block at row 0
   const double2* cblk = a.coef + chunk * kCoefBlk;
 
-  // lane 0: issue the copies of iteration j into slot s
-  auto issue = [&](int s, int j) {
+  // lane 0: the copies of iteration j into slot s.  The coefficient block
+  // does not depend on the previous stage; the state blocks do.
+  auto issue_coef = [&](int s, int j) {  // before pdl_wait: bytes expected, no arrival
+    const uint32_t bar = bar0 + s * 8;
+    mbar_expect_tx_only(bar, kCoefBlk * 16);
+    bulk_g2s(smem_u32(ring + (size_t)s * SB) + SlotT::COEF, cblk + j * crs, kCoefBlk * 16, bar);
+  };
+  auto issue_state = [&](int s, int j, bool with_coef) {
     const uint32_t bar = bar0 + s * 8;
     const uint32_t dst = smem_u32(ring + (size_t)s * SB);
     const int rn = j + 1 + R;
     const bool st = (j + 1 < je) && !(rn >= n && a.phys_hi);
-    const uint32_t bytes = SlotT::BYTES - (st ? 0 : kStateBlk * 16);
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(dst + SlotT::COEF, cblk + j * crs, kCoefBlk * 16, bar);
+    const uint32_t bytes =
+        SlotT::BYTES - (st ? 0 : kStateBlk * 16) - (with_coef ? 0 : kCoefBlk * 16);
+    mbar_expect_tx(bar, bytes);  // + the arrival that completes the phase
+    if (with_coef) bulk_g2s(dst + SlotT::COEF, cblk + j * crs, kCoefBlk * 16, bar);
     if (st) bulk_g2s(dst + SlotT::XN, xblk + rn * rs, kStateBlk * 16, bar);
     const ptrdiff_t o = j * rs + chunk * kStateBlk;
     if (SlotT::HAS_A) bulk_g2s(dst + SlotT::A, a.ua + o, kStateBlk * 16, bar);
@@ -583,11 +597,36 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
       bulk_g2s(dst + SlotT::G, a.ug + o, kStateBlk * 16, bar);
     }
   };
-  if (lane == 0) {
+  const int nq = live ? (je - jb < S ? je - jb : S) : 0;  // slots primed
+  // ---- prologue, overlapping the previous stage's tail (programmatic launch)
+  if (lane == 0 && live) {
     for (int s = 0; s < S; ++s) mbar_init(bar0 + s * 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int q = 0; q < S && jb + q < je; ++q) issue(q, jb + q);
+    for (int q = 0; q < nq; ++q) issue_coef(q, jb + q);
   }
+  pdl_wait();  // the previous stage's grid has completed; its writes are visible
+  if (a.flag != nullptr && *(volatile unsigned long long*)a.flag != 0ull) {  // frozen
+    if (lane == 0)
+      for (int q = 0; q < nq; ++q) {  // drain the coefficient copies before exiting
+        mbar_arrive(bar0 + q * 8);
+        mbar_wait(bar0 + q * 8, 0);
+      }
+    // a frozen slab still releases its neighbours for this stage (no data)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (a.px.on_lo | a.px.on_hi)) {
+      if (a.px.on_lo) peer_signal(a.px.sig_lo, (unsigned long long)a.nchunks);
+      if (a.px.on_hi) peer_signal(a.px.sig_hi, (unsigned long long)a.nchunks);
+      *a.px.epoch += 1ull;
+    }
+    return false;
+  }
+  if (a.bump && blockIdx.x == 0 && threadIdx.x == 0) a.flag[2] += 1ull;  // step counter
+  if (!live) return true;
+  // boundary ranges: wait for the neighbours' halo rows of this stage
+  if ((a.px.on_lo && range == 0) | (a.px.on_hi && range == a.nranges - 1))
+    peer_wait_halos(a.px.wait, a.px.epoch, a.flag, a.nchunks, a.px.timeout_ns,
+                    range == 0 && a.px.on_lo, range == a.nranges - 1 && a.px.on_hi);
+  if (lane == 0)
+    for (int q = 0; q < nq; ++q) issue_state(q, jb + q, false);
   __syncwarp();
 
   const double2* xps = xblk + lane;        // this lane's Psi at row 0
@@ -817,7 +856,7 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
     __syncwarp();
     if (lane == 0 && j + S < je) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(slot, j + S);
+      issue_state(slot, j + S, true);
     }
     if (++slot == S) { slot = 0; parity ^= 1u; }
   }
@@ -830,6 +869,7 @@ __device__ __forceinline__ void stage_body(const StageArgs& a) {
     // sees a half-frozen state
     atomicOr(a.flag + (a.tick != nullptr ? 3 : 0), 1ull);
   }
+  return true;
 }
 
 }  // namespace hwg

@@ -129,6 +129,7 @@ struct hwg_solver {
   };
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
+  bool use_pdl = true;       // programmatic dependent launch of the stage kernels
   // observers
   int kobs = -1, j0 = -1, jobs = -1;
   double* obs_w = nullptr;   // 32 horizon weights + ntheta projection weights
@@ -359,6 +360,7 @@ StageArgs base_args(const hwg_solver* s) {
   StageArgs a{};
   a.n = s->n; a.nt = s->nt; a.nchunks = s->nchunks;
   a.rs = (long long)s->rs; a.crs = (long long)s->crs;
+  a.pdl = s->use_pdl ? 1 : 0;
   a.phys_lo = s->phys_lo; a.phys_hi = s->phys_hi;
   a.nranges = s->nranges;
   a.negpar = s->d.parity < 0 ? 1 : 0;
@@ -780,6 +782,7 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   s->eps = {d->eps, ddm ? d->eps_lo : 0.0};
   s->sigma = {d->sigma, ddm ? d->sigma_lo : 0.0};
   if (const char* e = std::getenv("HWG_NO_GRAPH")) s->use_graphs = e[0] == '0';
+  if (const char* e = std::getenv("HWG_NO_PDL")) s->use_pdl = e[0] == '0';
   auto fail = [&](int rc) {
     g_create_err = s->err;
     hwg_destroy(s);

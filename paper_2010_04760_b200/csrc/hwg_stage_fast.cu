@@ -11,7 +11,25 @@ struct FastLauncher {
                          (int)stage_smem_bytes<EPI>());
   }
   static void run(const StageArgs& a, int blocks, int wpb, cudaStream_t st) {
-    stage_kernel<SCH, MODE, EPI><<<blocks, wpb * 32, stage_smem_bytes<EPI>(wpb), st>>>(a);
+    if (!a.pdl) {
+      stage_kernel<SCH, MODE, EPI><<<blocks, wpb * 32, stage_smem_bytes<EPI>(wpb), st>>>(a);
+      return;
+    }
+    // programmatic dependent launch: this stage's blocks may start (barrier
+    // set-up, coefficient prefetch) while the previous stage drains; the
+    // kernel waits for the previous grid (griddepcontrol.wait) before it
+    // reads any state
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(wpb * 32);
+    cfg.dynamicSmemBytes = stage_smem_bytes<EPI>(wpb);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, stage_kernel<SCH, MODE, EPI>, a);
   }
 };
 }  // namespace
