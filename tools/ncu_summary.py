@@ -78,9 +78,11 @@ def main():
         lines += ["", f"mean DRAM bytes per launch: {mean:.4e}"]
         open(os.path.join(ROOT, "profiles", f"{tag}_ncu_{name}.md"), "w").write(
             "\n".join(lines) + "\n")
-        # report names end in the tier: ..._mixed, ..._f64, ..._ddmixed, ..._ddfull
-        mode = name.rsplit("_", 1)[-1]
-        traffic[f"{mode}_65536x512"] = mean
+        # C5 captures are named <tag>_full_<tier> (tier: mixed, f64, ddmixed,
+        # ddfull); captures of other shapes do not feed bench.py's traffic
+        if "_full_" in name:
+            mode = name.rsplit("_", 1)[-1]
+            traffic[f"{mode}_65536x512"] = mean
         print(name, mean)
     json.dump(traffic, open(tfile, "w"), indent=1)
 
