@@ -45,7 +45,7 @@
 #define HWG_MINB_F64 3  // fp64 weights: 12 warps at up to 168 registers (measured faster)
 #endif
 #ifndef HWG_RING
-#define HWG_RING 3  // bulk-copy ring depth per warp
+#define HWG_RING 2  // bulk-copy ring depth per warp (measured: 2 beats 3 and 4 by 1-2 %)
 #endif
 
 namespace hwg {
