@@ -18,8 +18,17 @@
 
 #include "../../include/hweno_gpu.h"
 #include "hwg_launch.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for nsys / ncu --nvtx
 
 using namespace hwg;
+
+namespace {
+// NVTX range over a C-ABI entry point (no-op unless a profiler is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 thread_local std::string g_create_err;
@@ -905,11 +914,13 @@ const char* hwg_last_error(const hwg_solver* s) {
 }
 
 int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_solver** out) {
+  NvtxRange nvtx_("hwg_create");
   return create_impl(d, coef, nullptr, cotth, nullptr, false, out);
 }
 
 int hwg_create_dd(const hwg_desc* d, const double* coef_hi, const double* coef_lo,
                   const double* cot_hi, const double* cot_lo, hwg_solver** out) {
+  NvtxRange nvtx_("hwg_create_dd");
   return create_impl(d, coef_hi, coef_lo, cot_hi, cot_lo, true, out);
 }
 
@@ -958,6 +969,7 @@ int hwg_peer_export(hwg_solver* s, hwg_peer_desc* out) {
 
 int hwg_set_peers(hwg_solver* s, const hwg_peer_desc* lower, const hwg_peer_desc* upper,
                   int use_ipc, double timeout_s) {
+  NvtxRange nvtx_("hwg_set_peers");
   cudaSetDevice(s->dev);
   if (s->ddm) {
     s->err = "hwg_set_peers: fused halo push is implemented for the fp64 / mixed tiers";
@@ -1012,6 +1024,7 @@ int hwg_set_peers(hwg_solver* s, const hwg_peer_desc* lower, const hwg_peer_desc
 }
 
 int hwg_peer_prime(hwg_solver* s) {
+  NvtxRange nvtx_("hwg_peer_prime");
   cudaSetDevice(s->dev);
   const int h = halo_rows(s->d.scheme);
   const size_t bytes = (size_t)h * s->rs * sizeof(double2);
@@ -1032,6 +1045,7 @@ int hwg_set_stream(hwg_solver* s, void* stream, int own) {
 }
 
 int hwg_set_state_dd(hwg_solver* s, const double* u) {
+  NvtxRange nvtx_("hwg_set_state_dd");
   cudaSetDevice(s->dev);
   int rc = upload_layout(s, u, 2, s->cur);
   if (rc) return rc;
@@ -1040,6 +1054,7 @@ int hwg_set_state_dd(hwg_solver* s, const double* u) {
   return HWG_OK;
 }
 int hwg_set_state(hwg_solver* s, const double* u) {
+  NvtxRange nvtx_("hwg_set_state");
   cudaSetDevice(s->dev);
   int rc = upload_layout(s, u, 1, s->cur);
   if (rc) return rc;
@@ -1048,19 +1063,23 @@ int hwg_set_state(hwg_solver* s, const double* u) {
   return HWG_OK;
 }
 int hwg_get_state_dd(hwg_solver* s, double* u) {
+  NvtxRange nvtx_("hwg_get_state_dd");
   cudaSetDevice(s->dev);
   return download_layout(s, u, 2, s->cur, true);
 }
 int hwg_get_state(hwg_solver* s, double* u) {
+  NvtxRange nvtx_("hwg_get_state");
   cudaSetDevice(s->dev);
   return download_layout(s, u, 1, s->cur, true);
 }
 
 int hwg_rhs(hwg_solver* s, double* u, double* du) {
+  NvtxRange nvtx_("hwg_rhs");
   cudaSetDevice(s->dev);
   return rhs_impl(s, u, du, 1);
 }
 int hwg_rhs_dd(hwg_solver* s, double* u, double* du) {
+  NvtxRange nvtx_("hwg_rhs_dd");
   cudaSetDevice(s->dev);
   return rhs_impl(s, u, du, 2);
 }
@@ -1081,6 +1100,7 @@ int hwg_launch_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double
 
 int hwg_launch_steps(hwg_solver* s, int stepper, double dt_hi, double dt_lo,
                      long long step_begin, long long nsteps) {
+  NvtxRange nvtx_("hwg_launch_steps");
   cudaSetDevice(s->dev);
   return launch_steps_impl(s, stepper, dt_hi, dt_lo, step_begin, nsteps);
 }
@@ -1148,6 +1168,7 @@ int hwg_set_observers(hwg_solver* s, int kobs, int j0, const double* hw, int job
 }
 
 int hwg_observe(hwg_solver* s, hwg_observables* out) {
+  NvtxRange nvtx_("hwg_observe");
   observe_kernel2<<<1, 32, 0, s->stream>>>(row0(s, s->cur), s->rs, s->sblk, s->j0, s->obs_w,
                                             s->kobs, s->jobs, s->phys_hi ? s->n - 1 : -1,
                                             s->obs_w + 32, s->nt, s->obs_dev);
@@ -1167,6 +1188,7 @@ int hwg_observe(hwg_solver* s, hwg_observables* out) {
 int hwg_advance(hwg_solver* s, int stepper, double dt_hi, double dt_lo, long long s0,
                 long long s1, long long every, hwg_hook_fn hook, void* user,
                 hwg_run_stats* stats) {
+  NvtxRange nvtx_("hwg_advance");
   cudaSetDevice(s->dev);
   hwg_run_stats st{0, 0.0, 0, -1};
   if (every < 1) every = 1;
