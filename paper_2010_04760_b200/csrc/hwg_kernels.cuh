@@ -336,13 +336,6 @@ struct Win {
   static constexpr int IA = (IL + 4 > IW) ? IL + 4 : IW;  // + 4 rows for the cubic
 };
 
-__device__ __forceinline__ double2 shfl_up2(double2 v, int d) {
-  return make_double2(__shfl_up_sync(kFull, v.x, d), __shfl_up_sync(kFull, v.y, d));
-}
-__device__ __forceinline__ double2 shfl_dn2(double2 v, int d) {
-  return make_double2(__shfl_down_sync(kFull, v.x, d), __shfl_down_sync(kFull, v.y, d));
-}
-
 // parity reflection of a theta column across the poles (evolve.cpp:59-70)
 __device__ __forceinline__ int reflect_col(int c, int nt, bool& flip, int negpar) {
   flip = false;
