@@ -627,34 +627,35 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
 
   // ---- initial rows jb - IL .. jb + R (ghosts synthesised at the excision end)
   double2 ips[Wn::IA], ipi[Wn::IA];
-  if (a.phys_lo && jb < IL) {
-    // only jb == 0 happens (ranges are >= 8 rows)
+  // rows -IL .. 3 of the excision end when this range starts within IL rows
+  // of it: gs[IL + r] = row r, ghosts by the reference's recurrence
+  // (t = 1, 2, ... from rows 0..3)
+  const bool lo_ghosts = a.phys_lo && jb < IL;
+  double2 gs[IL + 4], gp[IL + 4];
+  if (lo_ghosts) {
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      ips[IL + m] = __ldcg(xps + m * rs);
-      ipi[IL + m] = __ldcg(xpi + m * rs);
+      gs[IL + m] = __ldcg(xps + m * rs);
+      gp[IL + m] = __ldcg(xpi + m * rs);
     }
 #pragma unroll
     for (int t = 1; t <= IL; ++t) {
-      ips[IL - t] = cubic(ips[IL - t + 1], ips[IL - t + 2], ips[IL - t + 3], ips[IL - t + 4]);
-      ipi[IL - t] = cubic(ipi[IL - t + 1], ipi[IL - t + 2], ipi[IL - t + 3], ipi[IL - t + 4]);
+      gs[IL - t] = cubic(gs[IL - t + 1], gs[IL - t + 2], gs[IL - t + 3], gs[IL - t + 4]);
+      gp[IL - t] = cubic(gp[IL - t + 1], gp[IL - t + 2], gp[IL - t + 3], gp[IL - t + 4]);
     }
+  }
 #pragma unroll
-    for (int m = IL + 4; m < IW; ++m) {
-      ips[m] = __ldcg(xps + (m - IL) * rs);
-      ipi[m] = __ldcg(xpi + (m - IL) * rs);
-    }
-  } else {
-#pragma unroll
-    for (int m = 0; m < IW; ++m) {
-      const int r = jb - IL + m;
-      if (r >= n && a.phys_hi) {
-        ips[m] = cubic(ips[m - 1], ips[m - 2], ips[m - 3], ips[m - 4]);
-        ipi[m] = cubic(ipi[m - 1], ipi[m - 2], ipi[m - 3], ipi[m - 4]);
-      } else {
-        ips[m] = __ldcg(xps + r * rs);
-        ipi[m] = __ldcg(xpi + r * rs);
-      }
+  for (int m = 0; m < IW; ++m) {
+    const int r = jb - IL + m;
+    if (lo_ghosts && r < 4) {
+      ips[m] = gs[IL + r];
+      ipi[m] = gp[IL + r];
+    } else if (m >= 4 && r >= n && a.phys_hi) {  // scri continuation (r >= n implies m >= 4)
+      ips[m] = cubic(ips[m - 1], ips[m - 2], ips[m - 3], ips[m - 4]);
+      ipi[m] = cubic(ipi[m - 1], ipi[m - 2], ipi[m - 3], ipi[m - 4]);
+    } else {
+      ips[m] = __ldcg(xps + r * rs);
+      ipi[m] = __ldcg(xpi + r * rs);
     }
   }
   double2 wps[SW], wpi[PW];

@@ -880,8 +880,11 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
     CK(ddm ? occupancy_dd(&occ) : occupancy_fast(&occ, mode_of(s)));
     const long long target = (long long)nsm * std::max(occ, 1) * kWarpsPerBlock;
     long long nr = std::max<long long>(1, target / s->nchunks);
-    int minrows = 4;  // rows per range (the window warm-up costs ~2 rows of work)
-    if (const char* e = std::getenv("HWG_MIN_ROWS")) minrows = std::max(4, std::atoi(e));
+    // rows per range: as few as 2 on tiny grids to fill the wave (the window
+    // warm-up costs ~2 rows of work, so larger grids keep longer ranges)
+    // (the double-double kernel's window set-up assumes ranges of >= 4 rows)
+    int minrows = ddm ? 4 : 2;
+    if (const char* e = std::getenv("HWG_MIN_ROWS")) minrows = std::max(minrows, std::atoi(e));
     nr = std::min<long long>(nr, std::max(1, s->n / minrows));
     s->nranges = (int)nr;
     // small grids: fewer warps per block so the warps spread over all SMs
