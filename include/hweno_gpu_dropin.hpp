@@ -125,14 +125,20 @@ struct HookCtx {
   GpuEvolutionRhs* rhs;
   const hweno::SampleHook* hook;
   hweno::StateVec* u;
+  std::exception_ptr err;  // thrown by the hook: rethrown once hwg_advance returns
 };
 inline void trampoline(long long step, double tau_hi, double tau_lo, const hwg_observables*,
-                       void* user) {
+                       void* user) noexcept {
   auto* c = static_cast<HookCtx*>(user);
-  // the reference hook sees the full state (driver.cpp:64-91): bring it back
-  check(hwg_get_state_dd(c->rhs->handle(), reinterpret_cast<double*>(c->u->data())),
-        c->rhs->handle());
-  c->hook->fn(long(step), hweno::WorkReal(tau_hi, tau_lo), *c->u);
+  try {
+    // the reference hook sees the full state (driver.cpp:64-91): bring it back
+    check(hwg_get_state_dd(c->rhs->handle(), reinterpret_cast<double*>(c->u->data())),
+          c->rhs->handle());
+    c->hook->fn(long(step), hweno::WorkReal(tau_hi, tau_lo), *c->u);
+  } catch (...) {  // no exception crosses the C ABI; stop the run as the reference would
+    c->err = std::current_exception();
+    hwg_abort_advance(c->rhs->handle());
+  }
 }
 }  // namespace detail
 
@@ -145,12 +151,14 @@ inline hweno::RunStats advance_steps(GpuEvolutionRhs& rhs, const hweno::StepperS
                                      const hweno::SampleHook& hook) {
   hwg_solver* h = rhs.handle();
   check(hwg_set_state_dd(h, reinterpret_cast<const double*>(u.data())), h);
-  detail::HookCtx ctx{&rhs, &hook, &u};
+  detail::HookCtx ctx{&rhs, &hook, &u, nullptr};
   hwg_run_stats st{};
   const int kind = stepper.kind == hweno::StepperSpec::ssprk33 ? HWG_SSPRK33 : HWG_SSPRK104;
-  check(hwg_advance(h, kind, dt.hi, dt.lo, step_begin, step_end, hook.fn ? hook.every : 1,
-                    hook.fn ? detail::trampoline : nullptr, &ctx, &st),
-        h);
+  const int rc = hwg_advance(h, kind, dt.hi, dt.lo, step_begin, step_end,
+                             hook.fn ? hook.every : 1, hook.fn ? detail::trampoline : nullptr,
+                             &ctx, &st);
+  if (ctx.err) std::rethrow_exception(ctx.err);  // the hook's own exception
+  check(rc, h);
   check(hwg_get_state_dd(h, reinterpret_cast<double*>(u.data())), h);
   hweno::RunStats rs;
   rs.steps_done = long(st.steps_done);

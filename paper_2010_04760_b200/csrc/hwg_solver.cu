@@ -139,6 +139,7 @@ struct hwg_solver {
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
   bool use_pdl = true;       // programmatic dependent launch of the stage kernels
+  bool abort_req = false;    // hwg_abort_advance called from the hook
   // observers
   int kobs = -1, j0 = -1, jobs = -1;
   double* obs_w = nullptr;   // 32 horizon weights + ntheta projection weights
@@ -910,6 +911,31 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
 }  // namespace
 
 // ----------------------------------------------------------------------------
+// No C++ exception crosses the C ABI: every entry point runs under
+// guarded(), which maps std::bad_alloc / std::exception to HWG_ERUNTIME
+// with the message in hwg_last_error (int status returns).
+template <class S>
+void set_err(S* s, const char* msg) noexcept {
+  try {
+    if (s) const_cast<hwg_solver*>(s)->err = msg;
+    else g_create_err = msg;
+  } catch (...) {
+  }
+}
+template <class S, class F>
+int guarded(S* s, F&& f) noexcept {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    set_err(s, "out of host memory");
+  } catch (const std::exception& e) {
+    set_err(s, e.what());
+  } catch (...) {
+    set_err(s, "unknown C++ exception");
+  }
+  return HWG_ERUNTIME;
+}
+
 extern "C" {
 
 const char* hwg_last_error(const hwg_solver* s) {
@@ -917,14 +943,18 @@ const char* hwg_last_error(const hwg_solver* s) {
 }
 
 int hwg_create(const hwg_desc* d, const double* coef, const double* cotth, hwg_solver** out) {
-  NvtxRange nvtx_("hwg_create");
-  return create_impl(d, coef, nullptr, cotth, nullptr, false, out);
+  return guarded(static_cast<hwg_solver*>(nullptr), [&]() -> int {
+    NvtxRange nvtx_("hwg_create");
+    return create_impl(d, coef, nullptr, cotth, nullptr, false, out);
+  });
 }
 
 int hwg_create_dd(const hwg_desc* d, const double* coef_hi, const double* coef_lo,
                   const double* cot_hi, const double* cot_lo, hwg_solver** out) {
-  NvtxRange nvtx_("hwg_create_dd");
-  return create_impl(d, coef_hi, coef_lo, cot_hi, cot_lo, true, out);
+  return guarded(static_cast<hwg_solver*>(nullptr), [&]() -> int {
+    NvtxRange nvtx_("hwg_create_dd");
+    return create_impl(d, coef_hi, coef_lo, cot_hi, cot_lo, true, out);
+  });
 }
 
 void hwg_destroy(hwg_solver* s) {
@@ -949,296 +979,344 @@ void hwg_destroy(hwg_solver* s) {
 }
 
 int hwg_peer_export(hwg_solver* s, hwg_peer_desc* out) {
-  cudaSetDevice(s->dev);
-  std::memset(out, 0, sizeof(*out));
-  int rc = ensure_regs(s, 5);
-  if (rc) return rc;
-  for (int i = 0; i < 5; ++i) {
-    out->reg[i] = s->reg[i];
+  return guarded(s, [&]() -> int {
+    cudaSetDevice(s->dev);
+    std::memset(out, 0, sizeof(*out));
+    int rc = ensure_regs(s, 5);
+    if (rc) return rc;
+    for (int i = 0; i < 5; ++i) {
+      out->reg[i] = s->reg[i];
+      cudaIpcMemHandle_t h;
+      CK(cudaIpcGetMemHandle(&h, s->reg[i]));
+      std::memcpy(out->ipc[i], &h, sizeof(h));
+    }
+    out->flag = s->flag;
     cudaIpcMemHandle_t h;
-    CK(cudaIpcGetMemHandle(&h, s->reg[i]));
-    std::memcpy(out->ipc[i], &h, sizeof(h));
-  }
-  out->flag = s->flag;
-  cudaIpcMemHandle_t h;
-  CK(cudaIpcGetMemHandle(&h, s->flag));
-  std::memcpy(out->ipc[5], &h, sizeof(h));
-  out->nrho = s->n;
-  out->row_elems = (long long)s->rs;
-  out->device = s->dev;
-  CK(cudaStreamSynchronize(s->stream));  // registers zeroed before anyone maps them
-  return HWG_OK;
+    CK(cudaIpcGetMemHandle(&h, s->flag));
+    std::memcpy(out->ipc[5], &h, sizeof(h));
+    out->nrho = s->n;
+    out->row_elems = (long long)s->rs;
+    out->device = s->dev;
+    CK(cudaStreamSynchronize(s->stream));  // registers zeroed before anyone maps them
+    return HWG_OK;
+  });
 }
 
 int hwg_set_peers(hwg_solver* s, const hwg_peer_desc* lower, const hwg_peer_desc* upper,
                   int use_ipc, double timeout_s) {
-  NvtxRange nvtx_("hwg_set_peers");
-  cudaSetDevice(s->dev);
-  if (s->ddm) {
-    s->err = "hwg_set_peers: fused halo push is implemented for the fp64 / mixed tiers";
-    return HWG_EINVAL;
-  }
-  if ((lower && s->phys_lo) || (upper && s->phys_hi)) {
-    s->err = "hwg_set_peers: a neighbour on a physical (excision / scri) end";
-    return HWG_EINVAL;
-  }
-  int rc = ensure_regs(s, 5);
-  if (rc) return rc;
-  CK(cudaStreamSynchronize(s->stream));
-  for (auto* p : {&s->plo, &s->phi}) {
-    for (void* m : p->opened) cudaIpcCloseMemHandle(m);
-    *p = hwg_solver::Peer{};
-  }
-  const hwg_peer_desc* ds[2] = {lower, upper};
-  hwg_solver::Peer* ps[2] = {&s->plo, &s->phi};
-  for (int q = 0; q < 2; ++q) {
-    const hwg_peer_desc* d = ds[q];
-    if (!d) continue;
-    if (d->row_elems != (long long)s->rs) {
-      s->err = "hwg_set_peers: neighbour row pitch differs (ntheta must match)";
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_set_peers");
+    cudaSetDevice(s->dev);
+    if (s->ddm) {
+      s->err = "hwg_set_peers: fused halo push is implemented for the fp64 / mixed tiers";
       return HWG_EINVAL;
     }
-    hwg_solver::Peer& p = *ps[q];
-    for (int i = 0; i < 6; ++i) {
-      void* ptr = i < 5 ? d->reg[i] : d->flag;
-      if (use_ipc) {
-        cudaIpcMemHandle_t h;
-        std::memcpy(&h, d->ipc[i], sizeof(h));
-        CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
-        p.opened.push_back(ptr);
-      } else if (d->device != s->dev) {
-        cudaError_t e = cudaDeviceEnablePeerAccess(d->device, 0);
-        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-        else CK(e);
-      }
-      if (i < 5) p.reg[i] = static_cast<double2*>(ptr);
-      else p.flag = static_cast<unsigned long long*>(ptr);
+    if ((lower && s->phys_lo) || (upper && s->phys_hi)) {
+      s->err = "hwg_set_peers: a neighbour on a physical (excision / scri) end";
+      return HWG_EINVAL;
     }
-    p.n = d->nrho;
-    p.on = true;
-  }
-  s->peer_timeout_ns = (long long)(timeout_s > 0 ? timeout_s * 1e9 : 10e9);
-  // counters, epoch and ticket restart at 0; graphs baked the old peer args
-  for (auto& e : s->graphs) cudaGraphExecDestroy(e.exec);
-  s->graphs.clear();
-  CK(cudaMemsetAsync(s->flag + 4, 0, 4 * sizeof(unsigned long long), s->stream));
-  CK(cudaStreamSynchronize(s->stream));
-  return HWG_OK;
+    int rc = ensure_regs(s, 5);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(s->stream));
+    for (auto* p : {&s->plo, &s->phi}) {
+      for (void* m : p->opened) cudaIpcCloseMemHandle(m);
+      *p = hwg_solver::Peer{};
+    }
+    const hwg_peer_desc* ds[2] = {lower, upper};
+    hwg_solver::Peer* ps[2] = {&s->plo, &s->phi};
+    for (int q = 0; q < 2; ++q) {
+      const hwg_peer_desc* d = ds[q];
+      if (!d) continue;
+      if (d->row_elems != (long long)s->rs) {
+        s->err = "hwg_set_peers: neighbour row pitch differs (ntheta must match)";
+        return HWG_EINVAL;
+      }
+      hwg_solver::Peer& p = *ps[q];
+      for (int i = 0; i < 6; ++i) {
+        void* ptr = i < 5 ? d->reg[i] : d->flag;
+        if (use_ipc) {
+          cudaIpcMemHandle_t h;
+          std::memcpy(&h, d->ipc[i], sizeof(h));
+          CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+          p.opened.push_back(ptr);
+        } else if (d->device != s->dev) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(d->device, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else CK(e);
+        }
+        if (i < 5) p.reg[i] = static_cast<double2*>(ptr);
+        else p.flag = static_cast<unsigned long long*>(ptr);
+      }
+      p.n = d->nrho;
+      p.on = true;
+    }
+    s->peer_timeout_ns = (long long)(timeout_s > 0 ? timeout_s * 1e9 : 10e9);
+    // counters, epoch and ticket restart at 0; graphs baked the old peer args
+    for (auto& e : s->graphs) cudaGraphExecDestroy(e.exec);
+    s->graphs.clear();
+    CK(cudaMemsetAsync(s->flag + 4, 0, 4 * sizeof(unsigned long long), s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return HWG_OK;
+  });
 }
 
 int hwg_peer_prime(hwg_solver* s) {
-  NvtxRange nvtx_("hwg_peer_prime");
-  cudaSetDevice(s->dev);
-  const int h = halo_rows(s->d.scheme);
-  const size_t bytes = (size_t)h * s->rs * sizeof(double2);
-  const int c = s->cur;
-  if (s->plo.on)
-    CK(cudaMemcpyAsync(s->plo.reg[c] + (size_t)(kHalo + s->plo.n) * s->rs, row0(s, c), bytes,
-                       cudaMemcpyDefault, s->stream));
-  if (s->phi.on)
-    CK(cudaMemcpyAsync(s->phi.reg[c] + (size_t)(kHalo - h) * s->rs, row0(s, c) + (size_t)(s->n - h) * s->rs,
-                       bytes, cudaMemcpyDefault, s->stream));
-  CK(cudaStreamSynchronize(s->stream));
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_peer_prime");
+    cudaSetDevice(s->dev);
+    const int h = halo_rows(s->d.scheme);
+    const size_t bytes = (size_t)h * s->rs * sizeof(double2);
+    const int c = s->cur;
+    if (s->plo.on)
+      CK(cudaMemcpyAsync(s->plo.reg[c] + (size_t)(kHalo + s->plo.n) * s->rs, row0(s, c), bytes,
+                         cudaMemcpyDefault, s->stream));
+    if (s->phi.on)
+      CK(cudaMemcpyAsync(s->phi.reg[c] + (size_t)(kHalo - h) * s->rs, row0(s, c) + (size_t)(s->n - h) * s->rs,
+                         bytes, cudaMemcpyDefault, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return HWG_OK;
+  });
 }
 
 int hwg_set_stream(hwg_solver* s, void* stream, int own) {
-  s->stream = own ? s->own : static_cast<cudaStream_t>(stream);
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    s->stream = own ? s->own : static_cast<cudaStream_t>(stream);
+    return HWG_OK;
+  });
 }
 
 int hwg_set_state_dd(hwg_solver* s, const double* u) {
-  NvtxRange nvtx_("hwg_set_state_dd");
-  cudaSetDevice(s->dev);
-  int rc = upload_layout(s, u, 2, s->cur);
-  if (rc) return rc;
-  CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
-  CK(cudaStreamSynchronize(s->stream));
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_set_state_dd");
+    cudaSetDevice(s->dev);
+    int rc = upload_layout(s, u, 2, s->cur);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return HWG_OK;
+  });
 }
 int hwg_set_state(hwg_solver* s, const double* u) {
-  NvtxRange nvtx_("hwg_set_state");
-  cudaSetDevice(s->dev);
-  int rc = upload_layout(s, u, 1, s->cur);
-  if (rc) return rc;
-  CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
-  CK(cudaStreamSynchronize(s->stream));
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_set_state");
+    cudaSetDevice(s->dev);
+    int rc = upload_layout(s, u, 1, s->cur);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    return HWG_OK;
+  });
 }
 int hwg_get_state_dd(hwg_solver* s, double* u) {
-  NvtxRange nvtx_("hwg_get_state_dd");
-  cudaSetDevice(s->dev);
-  return download_layout(s, u, 2, s->cur, true);
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_get_state_dd");
+    cudaSetDevice(s->dev);
+    return download_layout(s, u, 2, s->cur, true);
+  });
 }
 int hwg_get_state(hwg_solver* s, double* u) {
-  NvtxRange nvtx_("hwg_get_state");
-  cudaSetDevice(s->dev);
-  return download_layout(s, u, 1, s->cur, true);
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_get_state");
+    cudaSetDevice(s->dev);
+    return download_layout(s, u, 1, s->cur, true);
+  });
 }
 
 int hwg_rhs(hwg_solver* s, double* u, double* du) {
-  NvtxRange nvtx_("hwg_rhs");
-  cudaSetDevice(s->dev);
-  return rhs_impl(s, u, du, 1);
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_rhs");
+    cudaSetDevice(s->dev);
+    return rhs_impl(s, u, du, 1);
+  });
 }
 int hwg_rhs_dd(hwg_solver* s, double* u, double* du) {
-  NvtxRange nvtx_("hwg_rhs_dd");
-  cudaSetDevice(s->dev);
-  return rhs_impl(s, u, du, 2);
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_rhs_dd");
+    cudaSetDevice(s->dev);
+    return rhs_impl(s, u, du, 2);
+  });
 }
 
 int hwg_launch_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo,
                      long long step) {
-  if (stepper == HWG_SSPRK104) {
-    int rc = ensure_regs(s, 5);
-    if (rc) return rc;
-  }
-  const int ns = stepper == HWG_SSPRK33 ? 3 : 10;
-  if (stage < 0 || stage >= ns) {
-    s->err = "hwg_launch_stage: stage out of range";
-    return HWG_EINVAL;
-  }
-  return do_stage(s, stepper, stage, dt_hi, dt_lo, step);
+  return guarded(s, [&]() -> int {
+    if (stepper == HWG_SSPRK104) {
+      int rc = ensure_regs(s, 5);
+      if (rc) return rc;
+    }
+    const int ns = stepper == HWG_SSPRK33 ? 3 : 10;
+    if (stage < 0 || stage >= ns) {
+      s->err = "hwg_launch_stage: stage out of range";
+      return HWG_EINVAL;
+    }
+    return do_stage(s, stepper, stage, dt_hi, dt_lo, step);
+  });
 }
 
 int hwg_launch_steps(hwg_solver* s, int stepper, double dt_hi, double dt_lo,
                      long long step_begin, long long nsteps) {
-  NvtxRange nvtx_("hwg_launch_steps");
-  cudaSetDevice(s->dev);
-  return launch_steps_impl(s, stepper, dt_hi, dt_lo, step_begin, nsteps);
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_launch_steps");
+    cudaSetDevice(s->dev);
+    return launch_steps_impl(s, stepper, dt_hi, dt_lo, step_begin, nsteps);
+  });
 }
 
 int hwg_stage_input(const hwg_solver* s, int stepper, int stage, int* reg) {
-  *reg = stage_input_reg(s, stepper, stage);
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    *reg = stage_input_reg(s, stepper, stage);
+    return HWG_OK;
+  });
 }
 
 int hwg_register_ptr(const hwg_solver* s, int reg, void** row0_ptr, long long* row_elems) {
-  if (reg < 0 || reg >= s->nreg) return HWG_EINVAL;
-  *row0_ptr = row0(s, reg);
-  *row_elems = (long long)s->rs;
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    if (reg < 0 || reg >= s->nreg) return HWG_EINVAL;
+    *row0_ptr = row0(s, reg);
+    *row_elems = (long long)s->rs;
+    return HWG_OK;
+  });
 }
 
 int hwg_current_register(const hwg_solver* s) { return s->cur; }
 
 int hwg_status(hwg_solver* s, int* blew, long long* step, int clear) {
-  CK(cudaMemcpyAsync(s->hflag, s->flag, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                     s->stream));
-  CK(cudaStreamSynchronize(s->stream));
-  *blew = s->hflag[0] != 0;
-  *step = *blew ? (long long)s->hflag[1] : -1;
-  if (clear) {
-    CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
-    CK(cudaMemsetAsync(s->flag + 3, 0, sizeof(unsigned long long), s->stream));
-  }
-  if (s->hflag[0] & 2ull) {
-    s->err = "peer halo wait timed out (a neighbour slab did not run the same stage)";
-    return HWG_ERUNTIME;
-  }
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    CK(cudaMemcpyAsync(s->hflag, s->flag, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    *blew = s->hflag[0] != 0;
+    *step = *blew ? (long long)s->hflag[1] : -1;
+    if (clear) {
+      CK(cudaMemsetAsync(s->flag, 0, 2 * sizeof(unsigned long long), s->stream));
+      CK(cudaMemsetAsync(s->flag + 3, 0, sizeof(unsigned long long), s->stream));
+    }
+    if (s->hflag[0] & 2ull) {
+      s->err = "peer halo wait timed out (a neighbour slab did not run the same stage)";
+      return HWG_ERUNTIME;
+    }
+    return HWG_OK;
+  });
 }
 
 int hwg_launch_info(const hwg_solver* s, int* blocks, int* threads, int* nranges, int* nchunks,
                     int* pitch) {
-  *blocks = s->blocks;
-  *threads = s->wpb * 32;
-  *nranges = s->nranges;
-  *nchunks = s->nchunks;
-  *pitch = (int)s->rs;
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    *blocks = s->blocks;
+    *threads = s->wpb * 32;
+    *nranges = s->nranges;
+    *nchunks = s->nchunks;
+    *pitch = (int)s->rs;
+    return HWG_OK;
+  });
 }
 
 int hwg_synchronize(hwg_solver* s) {
-  CK(cudaStreamSynchronize(s->stream));
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    CK(cudaStreamSynchronize(s->stream));
+    return HWG_OK;
+  });
 }
 
 int hwg_set_observers(hwg_solver* s, int kobs, int j0, const double* hw, int jobs,
                       const double* pw) {
-  if (kobs >= s->nt || j0 + 8 > s->n || jobs >= s->n) {
-    s->err = "hwg_set_observers: observer outside this handle's rows";
-    return HWG_EINVAL;
-  }
-  s->kobs = kobs;
-  s->j0 = hw ? j0 : -1;
-  s->jobs = pw ? jobs : -1;
-  std::vector<double> w(32 + s->ntp, 0.0);
-  if (hw) std::memcpy(w.data(), hw, 32 * sizeof(double));
-  if (pw) std::memcpy(w.data() + 32, pw, s->nt * sizeof(double));
-  CK(cudaMemcpy(s->obs_w, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    if (kobs >= s->nt || j0 + 8 > s->n || jobs >= s->n) {
+      s->err = "hwg_set_observers: observer outside this handle's rows";
+      return HWG_EINVAL;
+    }
+    s->kobs = kobs;
+    s->j0 = hw ? j0 : -1;
+    s->jobs = pw ? jobs : -1;
+    std::vector<double> w(32 + s->ntp, 0.0);
+    if (hw) std::memcpy(w.data(), hw, 32 * sizeof(double));
+    if (pw) std::memcpy(w.data() + 32, pw, s->nt * sizeof(double));
+    CK(cudaMemcpy(s->obs_w, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return HWG_OK;
+  });
 }
 
 int hwg_observe(hwg_solver* s, hwg_observables* out) {
-  NvtxRange nvtx_("hwg_observe");
-  observe_kernel2<<<1, 32, 0, s->stream>>>(row0(s, s->cur), s->rs, s->sblk, s->j0, s->obs_w,
-                                            s->kobs, s->jobs, s->phys_hi ? s->n - 1 : -1,
-                                            s->obs_w + 32, s->nt, s->obs_dev);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(s->obs_host, s->obs_dev, 14 * sizeof(double), cudaMemcpyDeviceToHost,
-                     s->stream));
-  CK(cudaStreamSynchronize(s->stream));
-  const double* o = s->obs_host;
-  out->phi[0] = o[0]; out->phi[1] = o[1];
-  for (int d = 0; d < 3; ++d) { out->dphi[d][0] = o[2 + 2 * d]; out->dphi[d][1] = o[3 + 2 * d]; }
-  out->obs[0] = o[8]; out->obs[1] = o[9];
-  out->scri[0] = o[10]; out->scri[1] = o[11];
-  out->proj[0] = o[12]; out->proj[1] = o[13];
-  return HWG_OK;
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_observe");
+    observe_kernel2<<<1, 32, 0, s->stream>>>(row0(s, s->cur), s->rs, s->sblk, s->j0, s->obs_w,
+                                              s->kobs, s->jobs, s->phys_hi ? s->n - 1 : -1,
+                                              s->obs_w + 32, s->nt, s->obs_dev);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->obs_host, s->obs_dev, 14 * sizeof(double), cudaMemcpyDeviceToHost,
+                       s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+    const double* o = s->obs_host;
+    out->phi[0] = o[0]; out->phi[1] = o[1];
+    for (int d = 0; d < 3; ++d) { out->dphi[d][0] = o[2 + 2 * d]; out->dphi[d][1] = o[3 + 2 * d]; }
+    out->obs[0] = o[8]; out->obs[1] = o[9];
+    out->scri[0] = o[10]; out->scri[1] = o[11];
+    out->proj[0] = o[12]; out->proj[1] = o[13];
+    return HWG_OK;
+  });
 }
 
 int hwg_advance(hwg_solver* s, int stepper, double dt_hi, double dt_lo, long long s0,
                 long long s1, long long every, hwg_hook_fn hook, void* user,
                 hwg_run_stats* stats) {
-  NvtxRange nvtx_("hwg_advance");
-  cudaSetDevice(s->dev);
-  hwg_run_stats st{0, 0.0, 0, -1};
-  if (every < 1) every = 1;
-  const long long poll = 256;
-  auto t0 = std::chrono::steady_clock::now();
-  int rc = HWG_OK;
-  long long launched_to = s0;  // steps [s0, launched_to) are queued
-  auto check_flag = [&](bool& blown) -> int {
-    int b;
-    long long bs;
-    int r = hwg_status(s, &b, &bs, 0);
-    if (r) return r;
-    blown = b != 0;
-    if (blown) {
-      st.blew_up = 1;
-      st.blowup_step = bs;
-      st.steps_done = bs - s0;
+  return guarded(s, [&]() -> int {
+    NvtxRange nvtx_("hwg_advance");
+    cudaSetDevice(s->dev);
+    s->abort_req = false;
+    hwg_run_stats st{0, 0.0, 0, -1};
+    if (every < 1) every = 1;
+    const long long poll = 256;
+    auto t0 = std::chrono::steady_clock::now();
+    int rc = HWG_OK;
+    long long launched_to = s0;  // steps [s0, launched_to) are queued
+    auto check_flag = [&](bool& blown) -> int {
+      int b;
+      long long bs;
+      int r = hwg_status(s, &b, &bs, 0);
+      if (r) return r;
+      blown = b != 0;
+      if (blown) {
+        st.blew_up = 1;
+        st.blowup_step = bs;
+        st.steps_done = bs - s0;
+      }
+      return HWG_OK;
+    };
+    long long q = s0;
+    for (;;) {
+      const bool hook_now = hook && (q % every == 0 || q == s0 || q == s1);
+      if (hook_now || q == s1 || (q - s0) % poll == 0) {
+        bool blown = false;
+        if ((rc = check_flag(blown))) break;
+        if (blown) break;
+      }
+      if (hook_now) {
+        hwg_observables ob;
+        if ((rc = hwg_observe(s, &ob))) break;
+        DD tau = tau_of(q, dt_hi, dt_lo);
+        hook(q, tau.hi, tau.lo, &ob, user);
+        if (s->abort_req) break;
+      }
+      if (q == s1) break;
+      // next stop: hook step, poll point or the end
+      long long next = std::min(s1, s0 + ((q - s0) / poll + 1) * poll);
+      if (hook) next = std::min(next, (q / every + 1) * every);
+      if ((rc = launch_steps_impl(s, stepper, dt_hi, dt_lo, q, next - q))) break;
+      launched_to = next;
+      st.steps_done = launched_to - s0;
+      q = next;
     }
-    return HWG_OK;
-  };
-  long long q = s0;
-  for (;;) {
-    const bool hook_now = hook && (q % every == 0 || q == s0 || q == s1);
-    if (hook_now || q == s1 || (q - s0) % poll == 0) {
-      bool blown = false;
-      if ((rc = check_flag(blown))) break;
-      if (blown) break;
-    }
-    if (hook_now) {
-      hwg_observables ob;
-      if ((rc = hwg_observe(s, &ob))) break;
-      DD tau = tau_of(q, dt_hi, dt_lo);
-      hook(q, tau.hi, tau.lo, &ob, user);
-    }
-    if (q == s1) break;
-    // next stop: hook step, poll point or the end
-    long long next = std::min(s1, s0 + ((q - s0) / poll + 1) * poll);
-    if (hook) next = std::min(next, (q / every + 1) * every);
-    if ((rc = launch_steps_impl(s, stepper, dt_hi, dt_lo, q, next - q))) break;
-    launched_to = next;
-    st.steps_done = launched_to - s0;
-    q = next;
-  }
-  cudaStreamSynchronize(s->stream);
-  st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  if (stats) *stats = st;
-  return rc;
+    cudaStreamSynchronize(s->stream);
+    st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (stats) *stats = st;
+    return rc;
+  });
+}
+
+int hwg_abort_advance(hwg_solver* s) {
+  if (s == nullptr) return HWG_EINVAL;
+  s->abort_req = true;
+  return HWG_OK;
 }
 
 }  // extern "C"

@@ -71,6 +71,7 @@ for _f in ("hwg_set_state_dd", "hwg_get_state_dd", "hwg_set_state", "hwg_get_sta
     getattr(_lib, _f).argtypes = [_vp, _dp]
 _lib.hwg_rhs.argtypes = [_vp, _dp, _dp]
 _lib.hwg_rhs_dd.argtypes = [_vp, _dp, _dp]
+_lib.hwg_abort_advance.argtypes = [_vp]
 _lib.hwg_advance.argtypes = [_vp, C.c_int, C.c_double, C.c_double, C.c_longlong, C.c_longlong,
                              C.c_longlong, HOOK, _vp, C.POINTER(HwgRunStats)]
 _lib.hwg_set_observers.argtypes = [_vp, C.c_int, C.c_int, _dp, C.c_int, _dp]
@@ -101,7 +102,7 @@ EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg
             "hwg_advance", "hwg_set_observers", "hwg_observe", "hwg_launch_stage",
             "hwg_launch_steps", "hwg_stage_input", "hwg_register_ptr",
             "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize",
-            "hwg_peer_export", "hwg_set_peers", "hwg_peer_prime"]
+            "hwg_peer_export", "hwg_set_peers", "hwg_peer_prime", "hwg_abort_advance"]
 
 
 class HwgError(RuntimeError):
@@ -256,6 +257,7 @@ class GpuEvolution:
                 hook(int(step), (thi, tlo), obs.contents.as_dict())
             except Exception as e:  # noqa: BLE001 - re-raised below
                 errors.append(e)
+                _lib.hwg_abort_advance(self.h)  # leave advance_steps now, as the reference does
 
         cb = HOOK(_cb) if hook is not None else HOOK()
         self._chk(_lib.hwg_advance(self.h, STEPPERS[stepper], dt_hi, dt_lo, step_begin, step_end,

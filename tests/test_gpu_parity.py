@@ -122,6 +122,28 @@ def test_hook_cadence_and_restart(cuda_ok):
     assert st["steps_done"] == 4 and seen == [10, 12, 14]
 
 
+def test_hook_exception_stops_the_run(cuda_ok):
+    """An exception thrown by the hook leaves advance_steps at once (the
+    reference's hook runs inside its loop, evolve.cpp:245-260): no further
+    step runs, the state is the one the hook saw, and the exception reaches
+    the caller (hwg_abort_advance; no C++ exception crosses the C ABI)."""
+    g = load_golden("extremal_w5")
+    dt = (float(g["dt"][0]), float(g["dt"][1]))
+    gpu = gpu_from_golden(g, "f64")
+    gpu.set_state(g["u0"])
+
+    def hook(s, tau, ob):
+        if s == 3:
+            raise KeyError("stop at 3")
+
+    with pytest.raises(KeyError):
+        gpu.advance("ssprk33", dt, 0, 10, every=1, hook=hook)
+    ref = gpu_from_golden(g, "f64")
+    ref.set_state(g["u0"])
+    ref.advance("ssprk33", dt, 0, 3)
+    assert np.array_equal(gpu.get_state(), ref.get_state())
+
+
 def test_blowup_freezes_state(cuda_ok):
     """proj/tests/test_evolve.cpp:352-361 and evolve.cpp:253-258."""
     g = load_golden("extremal_w5")
