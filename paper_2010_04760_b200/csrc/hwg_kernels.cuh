@@ -39,10 +39,9 @@
 #include <stdint.h>
 
 #ifndef HWG_MINB
-#define HWG_MINB 4  // resident blocks per SM (16 warps): caps registers at 128
-#endif
-#ifndef HWG_MINB_F64
-#define HWG_MINB_F64 3  // fp64 weights: 12 warps at up to 168 registers (measured faster)
+// resident blocks per SM: 3 (12 warps at up to 168 registers, room for the
+// 2-row unrolled loop) measured 2-4 % faster than 4 (16 warps at 128)
+#define HWG_MINB 3
 #endif
 #ifndef HWG_RING
 #define HWG_RING 2  // bulk-copy ring depth per warp (measured: 2 beats 3 and 4 by 1-2 %)
@@ -515,7 +514,7 @@ template <int SCH, int MODE, int EPI>
 __device__ __forceinline__ bool stage_body(const StageArgs& a);
 
 template <int SCH, int MODE, int EPI>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MODE == F64 ? HWG_MINB_F64 : HWG_MINB)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_MINB)
 stage_kernel(const StageArgs a) {
   if (!stage_body<SCH, MODE, EPI>(a)) return;  // frozen
   // let the next stage's grid launch once this warp's rows are done (measured:
@@ -680,12 +679,11 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
   int slot = 0;
   uint32_t parity = 0;
   // rows per unrolled iteration: 2 lets the register windows rotate with half
-  // the moves; measured +1.5 % for the fp64 tier (168 registers), -4 % for
-  // the 128-register mixed tier
+  // the moves (measured +1.5-4 % at 168 registers; 3 and 4 are slower)
 #ifdef HWG_UNROLL
   constexpr int kUnroll = HWG_UNROLL;
 #else
-  constexpr int kUnroll = (SCH == WENO5 && MODE == F64) ? 2 : 1;
+  constexpr int kUnroll = SCH == WENO5 ? 2 : 1;
 #endif
 #pragma unroll kUnroll
   for (int j = jb; j < je; ++j) {
