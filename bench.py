@@ -211,7 +211,10 @@ def make_runner(args, g, mode, rank, world, dist):
         print(f"[bench rank {rank}] no peer mappings ({r.error}); NCCL halos", file=sys.stderr)
         if r.error is None:
             g.set_peers(None, None)
-    return slabs.DistSlab(g, rank, world, "weno5"), ("nccl" if world > 1 else "none")
+    # NCCL P2P with the exchange overlapped with the interior rows (fast tiers)
+    overlap = not mode.startswith("dd")
+    return (slabs.DistSlab(g, rank, world, "weno5", overlap=overlap),
+            ("nccl-overlap" if overlap else "nccl") if world > 1 else "none")
 
 
 def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmup=None,
@@ -249,7 +252,7 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
             g.set_peers(None, None)
             g.status(clear=True)
             g.set_state(u0)
-            runner, halo = slabs.DistSlab(g, rank, world, "weno5"), "nccl"
+            runner, halo = slabs.DistSlab(g, rank, world, "weno5", overlap=True), "nccl-overlap"
             for q in range(W):
                 runner.step(stepper, dt, q)
             torch.cuda.synchronize()

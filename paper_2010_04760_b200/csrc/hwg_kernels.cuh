@@ -117,6 +117,10 @@ struct StageArgs {
   unsigned long long* tick;
   PeerArgs px;                     // fused halo push to the neighbour slabs (NVLink P2P)
   int pdl;                         // launched with programmatic stream serialisation
+  // row window of this launch: [row_lo, row_hi) of the slab (the whole slab,
+  // or one part of a stage split around an overlapped halo exchange)
+  int row_lo, row_hi;
+  int defer;                       // not the stage's last part: blow-up bit stays pending
 };
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
@@ -542,8 +546,9 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
   const int chunk = gw % a.nchunks;
   const int range = gw / a.nchunks;
   const bool live = range < a.nranges;  // else the whole warp only takes its ticket
-  const int jb = (int)((long long)range * a.n / a.nranges);
-  const int je = (int)((long long)(range + 1) * a.n / a.nranges);
+  const int span = a.row_hi - a.row_lo;
+  const int jb = a.row_lo + (int)((long long)range * span / a.nranges);
+  const int je = a.row_lo + (int)((long long)(range + 1) * span / a.nranges);
   const int k0 = chunk << 5;
   const int k = k0 + lane;
   const int nt = a.nt, n = a.n;
@@ -868,7 +873,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
     atomicExch(a.flag + 1, a.step >= 0 ? (unsigned long long)a.step : a.flag[2]);
     // published by the launch's last warp (tick) so no block of this launch
     // sees a half-frozen state
-    atomicOr(a.flag + (a.tick != nullptr ? 3 : 0), 1ull);
+    atomicOr(a.flag + (a.tick != nullptr || a.defer ? 3 : 0), 1ull);
   }
   return true;
 }

@@ -330,8 +330,9 @@ int mode_of(const hwg_solver* s) {
   return mixed ? MIXED : F64;
 }
 
-int launch(hwg_solver* s, const StageArgs& a, int epi) {
-  launch_stage_fast(a, s->d.scheme, mode_of(s), epi, s->blocks, s->wpb, s->stream);
+int launch(hwg_solver* s, const StageArgs& a, int epi, int blocks = 0) {
+  launch_stage_fast(a, s->d.scheme, mode_of(s), epi, blocks > 0 ? blocks : s->blocks, s->wpb,
+                    s->stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     s->err = std::string("stage launch: ") + cudaGetErrorString(e);
@@ -371,6 +372,9 @@ StageArgs base_args(const hwg_solver* s) {
   a.n = s->n; a.nt = s->nt; a.nchunks = s->nchunks;
   a.rs = (long long)s->rs; a.crs = (long long)s->crs;
   a.pdl = s->use_pdl ? 1 : 0;
+  a.row_lo = 0;
+  a.row_hi = s->n;
+  a.defer = 0;
   a.phys_lo = s->phys_lo; a.phys_hi = s->phys_hi;
   a.nranges = s->nranges;
   a.negpar = s->d.parity < 0 ? 1 : 0;
@@ -494,10 +498,22 @@ int halo_rows(int scheme) { return scheme == HWG_WENO5 ? 3 : scheme == HWG_WENO3
 
 // step >= 0: the kernel records step + 1 on blow-up; step < 0: counter mode
 // (flag[2] is bumped by stage 0 and recorded by the scan) for graph replay
+// One stage, or one part of it: rows [row_lo, row_hi) (fast tiers; the
+// double-double tiers always run whole stages).  `first`: the part that
+// bumps the device step counter; `last`: the part that publishes the blow-up
+// bit and rotates the registers.
+int do_stage_part(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo,
+                  long long step, int row_lo, int row_hi, bool first, bool last);
+
 int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, long long step) {
+  return do_stage_part(s, stepper, stage, dt_hi, dt_lo, step, 0, s->n, true, true);
+}
+
+int do_stage_part(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo,
+                  long long step, int row_lo, int row_hi, bool first, bool last) {
   const Plan p = make_plan(s, stepper, stage, DD{dt_hi, dt_lo});
   const long long rec = step >= 0 ? step + 1 : -1;
-  const int bump = (step < 0 && stage == 0) ? 1 : 0;
+  const int bump = (step < 0 && stage == 0 && first) ? 1 : 0;
   int rc;
   auto r0 = [&](int r) -> double2* { return r >= 0 ? row0(s, r) : nullptr; };
   if (s->ddm) {
@@ -534,11 +550,21 @@ int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, 
         x.sig_hi = s->phi.flag + 6;
       }
     }
-    if (check || s->plo.on || s->phi.on) a.tick = s->flag + 4;
-    rc = launch(s, a, p.epi);
+    int blocks = 0;
+    if (row_lo != 0 || row_hi != s->n) {  // a part: ranges in proportion to its rows
+      a.row_lo = row_lo;
+      a.row_hi = row_hi;
+      const int span = row_hi - row_lo;
+      a.nranges = (int)std::max<long long>(
+          1, std::min<long long>((long long)s->nranges * span / s->n, span / 2));
+      blocks = (int)(((long long)a.nranges * s->nchunks + s->wpb - 1) / s->wpb);
+    }
+    if (last && (check || s->plo.on || s->phi.on)) a.tick = s->flag + 4;
+    if (!last && check) a.defer = 1;
+    rc = launch(s, a, p.epi, blocks);
   }
-  if (p.rot == 1) std::swap(s->cur, s->scr1);
-  if (p.rot == 2) std::swap(s->cur, s->scr2);
+  if (last && p.rot == 1) std::swap(s->cur, s->scr1);
+  if (last && p.rot == 2) std::swap(s->cur, s->scr2);
   return rc;
 }
 
@@ -1310,6 +1336,27 @@ int hwg_advance(hwg_solver* s, int stepper, double dt_hi, double dt_lo, long lon
     st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (stats) *stats = st;
     return rc;
+  });
+}
+
+int hwg_launch_stage_rows(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo,
+                          long long step, int row_lo, int row_hi, int part) {
+  return guarded(s, [&]() -> int {
+    if (s->ddm || s->plo.on || s->phi.on) {
+      s->err = "hwg_launch_stage_rows: fast tiers without peer slabs only";
+      return HWG_EINVAL;
+    }
+    const int ns = stepper == HWG_SSPRK33 ? 3 : 10;
+    if (stage < 0 || stage >= ns || row_lo < 0 || row_hi > s->n || row_hi - row_lo < 2) {
+      s->err = "hwg_launch_stage_rows: stage or row window out of range";
+      return HWG_EINVAL;
+    }
+    if (stepper == HWG_SSPRK104) {
+      int rc = ensure_regs(s, 5);
+      if (rc) return rc;
+    }
+    return do_stage_part(s, stepper, stage, dt_hi, dt_lo, step, row_lo, row_hi,
+                         (part & HWG_PART_FIRST) != 0, (part & HWG_PART_LAST) != 0);
   });
 }
 

@@ -72,6 +72,8 @@ for _f in ("hwg_set_state_dd", "hwg_get_state_dd", "hwg_set_state", "hwg_get_sta
 _lib.hwg_rhs.argtypes = [_vp, _dp, _dp]
 _lib.hwg_rhs_dd.argtypes = [_vp, _dp, _dp]
 _lib.hwg_abort_advance.argtypes = [_vp]
+_lib.hwg_launch_stage_rows.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double,
+                                       C.c_longlong, C.c_int, C.c_int, C.c_int]
 _lib.hwg_advance.argtypes = [_vp, C.c_int, C.c_double, C.c_double, C.c_longlong, C.c_longlong,
                              C.c_longlong, HOOK, _vp, C.POINTER(HwgRunStats)]
 _lib.hwg_set_observers.argtypes = [_vp, C.c_int, C.c_int, _dp, C.c_int, _dp]
@@ -102,7 +104,8 @@ EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg
             "hwg_advance", "hwg_set_observers", "hwg_observe", "hwg_launch_stage",
             "hwg_launch_steps", "hwg_stage_input", "hwg_register_ptr",
             "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize",
-            "hwg_peer_export", "hwg_set_peers", "hwg_peer_prime", "hwg_abort_advance"]
+            "hwg_peer_export", "hwg_set_peers", "hwg_peer_prime", "hwg_abort_advance",
+            "hwg_launch_stage_rows"]
 
 
 class HwgError(RuntimeError):
@@ -282,6 +285,13 @@ class GpuEvolution:
     def launch_stage(self, stepper: str, stage: int, dt, step: int):
         dt_hi, dt_lo = (dt if isinstance(dt, tuple) else (float(dt), 0.0))
         self._chk(_lib.hwg_launch_stage(self.h, STEPPERS[stepper], stage, dt_hi, dt_lo, step))
+
+    def launch_stage_rows(self, stepper: str, stage: int, dt, step: int, row_lo: int,
+                          row_hi: int, first: bool, last: bool):
+        """One part of a stage: rows [row_lo, row_hi) (hwg_launch_stage_rows)."""
+        dt_hi, dt_lo = (dt if isinstance(dt, tuple) else (float(dt), 0.0))
+        self._chk(_lib.hwg_launch_stage_rows(self.h, STEPPERS[stepper], stage, dt_hi, dt_lo, step,
+                                             row_lo, row_hi, int(first) | 2 * int(last)))
 
     def launch_steps(self, stepper: str, dt, step_begin: int, nsteps: int):
         dt_hi, dt_lo = (dt if isinstance(dt, tuple) else (float(dt), 0.0))

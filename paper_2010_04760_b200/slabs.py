@@ -19,7 +19,10 @@ Transports:
                  (same-device pointers; on one GPU the slabs' stages are
                  launched in order, so every wait is already satisfied);
   * DistSlab   — torch.distributed point-to-point (NCCL over NVLink on GPUs,
-                 gloo on CPU), one process per GPU: the collective baseline;
+                 gloo on CPU), one process per GPU: the collective baseline.
+                 With overlap=True the exchange is posted,
+                 the interior rows [h, n-h) — which need no halo — run while
+                 it is in flight, then the two h-row boundary strips;
   * LocalSlabs — several handles in one process, halos copied with
                  stream-ordered device copies (bit-identity checks on one GPU).
 """
@@ -52,18 +55,23 @@ def halo_views(backend, reg: int, h: int):
 class DistSlab:
     """One rank's slab; halos through torch.distributed P2P."""
 
-    def __init__(self, backend, rank: int, world: int, scheme: str = "weno5", group=None):
+    def __init__(self, backend, rank: int, world: int, scheme: str = "weno5", group=None,
+                 overlap: bool = False):
         self.b = backend
         self.rank, self.world = rank, world
         self.left = rank - 1 if rank > 0 else None
         self.right = rank + 1 if rank < world - 1 else None
         self.h = HALO_ROWS[scheme]
         self.group = group
+        # interior / strips need >= 2 rows each (hwg_launch_stage_rows)
+        self.overlap = (overlap and world > 1 and hasattr(backend, "launch_stage_rows")
+                        and backend.nrho >= 2 * self.h + 2)
 
-    def exchange(self, reg: int):
+    def post(self, reg: int):
+        """Post the halo exchange of register `reg`; returns the requests."""
         import torch.distributed as dist
         if self.world == 1:
-            return
+            return []
         sl, rl, sr, rr = halo_views(self.b, reg, self.h)
         ops = []
         if self.left is not None:
@@ -72,14 +80,30 @@ class DistSlab:
         if self.right is not None:
             ops.append(dist.P2POp(dist.isend, sr, self.right, self.group))
             ops.append(dist.P2POp(dist.irecv, rr, self.right, self.group))
-        for req in dist.batch_isend_irecv(ops):
+        return dist.batch_isend_irecv(ops)
+
+    def exchange(self, reg: int):
+        for req in self.post(reg):
             req.wait()
 
     def step(self, stepper: str, dt, step: int):
         ns = 3 if stepper == "ssprk33" else 10
+        n, h = self.b.nrho, self.h
         for st in range(ns):
-            self.exchange(self.b.stage_input(stepper, st))
-            self.b.launch_stage(stepper, st, dt, step)
+            reqs = self.post(self.b.stage_input(stepper, st))
+            if not self.overlap:
+                for req in reqs:
+                    req.wait()
+                self.b.launch_stage(stepper, st, dt, step)
+                continue
+            # interior rows while the halo rows are in flight (NCCL: the
+            # kernel is queued behind nothing but the previous stage; wait()
+            # then orders the strips after the exchange on the device)
+            self.b.launch_stage_rows(stepper, st, dt, step, h, n - h, True, False)
+            for req in reqs:
+                req.wait()
+            self.b.launch_stage_rows(stepper, st, dt, step, 0, h, False, False)
+            self.b.launch_stage_rows(stepper, st, dt, step, n - h, n, False, True)
 
     def steps(self, stepper: str, dt, step_begin: int, nsteps: int):
         for q in range(nsteps):
@@ -162,11 +186,15 @@ class LocalPeerSlabs:
 
 
 class LocalSlabs:
-    """Several slab handles in one process (one GPU or CPU backends)."""
+    """Several slab handles in one process (one GPU or CPU backends).  With
+    overlap=True every stage runs as DistSlab's overlapped sequence: interior
+    parts, then the halo copies (so the interior parts see the previous
+    stage's halo rows — a dependence on them would show), then the strips."""
 
-    def __init__(self, backends, scheme: str = "weno5"):
+    def __init__(self, backends, scheme: str = "weno5", overlap: bool = False):
         self.bs = list(backends)
         self.h = HALO_ROWS[scheme]
+        self.overlap = overlap
 
     def exchange(self, regs):
         views = [halo_views(b, r, self.h) for b, r in zip(self.bs, regs)]
@@ -178,10 +206,19 @@ class LocalSlabs:
 
     def step(self, stepper: str, dt, step: int):
         ns = 3 if stepper == "ssprk33" else 10
+        h = self.h
         for st in range(ns):
-            self.exchange([b.stage_input(stepper, st) for b in self.bs])
+            regs = [b.stage_input(stepper, st) for b in self.bs]
+            if self.overlap:
+                for b in self.bs:
+                    b.launch_stage_rows(stepper, st, dt, step, h, b.nrho - h, True, False)
+            self.exchange(regs)
             for b in self.bs:
-                b.launch_stage(stepper, st, dt, step)
+                if self.overlap:
+                    b.launch_stage_rows(stepper, st, dt, step, 0, h, False, False)
+                    b.launch_stage_rows(stepper, st, dt, step, b.nrho - h, b.nrho, False, True)
+                else:
+                    b.launch_stage(stepper, st, dt, step)
 
     def steps(self, stepper: str, dt, step_begin: int, nsteps: int):
         for q in range(nsteps):

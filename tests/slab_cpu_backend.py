@@ -64,13 +64,19 @@ class CpuSlab:
         assert stepper == "ssprk33"
         return (self.cur, self.scr1, self.scr2)[stage]
 
-    def _rhs(self, reg: int) -> np.ndarray:
-        """F of the slab interior from register `reg` (halo rows valid)."""
+    def _rhs(self, reg: int, poison_halo: bool = False) -> np.ndarray:
+        """F of the slab interior from register `reg` (halo rows valid, or
+        replaced by NaN in a copy when they may still be in flight)."""
         g = self.g
         lo = 0 if self.off == 0 else 3
         hi = 0 if self.off + self.nrho == self.nglob else 3
         r0, r1 = self.off - lo, self.off + self.nrho + hi
         ext = from_rows(self.regs[reg][HALO - lo:HALO + self.nrho + hi].numpy(), self.nt)
+        if poison_halo:
+            if lo:
+                ext[:, :, :lo] = np.nan
+            if hi:
+                ext[:, :, -hi:] = np.nan
         m = r1 - r0
         coef = g["coef"].reshape(9, self.nt, self.nglob)[:, :, r0:r1]
         orc = OracleSolver(m, self.nt, float(g["drho"]), float(g["dtheta"]), int(g["parity"]),
@@ -82,10 +88,26 @@ class CpuSlab:
         return du[:, 2:-2, 4 + lo:4 + lo + self.nrho]
 
     def launch_stage(self, stepper: str, stage: int, dt, step: int):
-        # ssprk33_step (proj/include/hweno/timestep.hpp:54-71), interior only
+        self.launch_stage_rows(stepper, stage, dt, step, 0, self.nrho, True, True)
+
+    def launch_stage_rows(self, stepper: str, stage: int, dt, step: int, row_lo: int,
+                          row_hi: int, first: bool, last: bool):
+        """hwg_launch_stage_rows: write output rows [row_lo, row_hi) only;
+        rotate the registers on the stage's last part.  A part launched
+        while its halo rows are still in flight must not depend on them: the
+        halo rows are replaced by NaN (in the copy the stage reads) unless the
+        part touches a slab end (then the exchange has completed,
+        DistSlab.step)."""
         dt = dt[0] if isinstance(dt, tuple) else dt
         x = self.stage_input(stepper, stage)
-        f = self._rhs(x)
+        self._stage(stepper, stage, dt, x, row_lo, row_hi,
+                    poison=row_lo >= 3 and row_hi <= self.nrho - 3)
+        if last and stage == 2:
+            self.cur, self.scr1 = self.scr1, self.cur
+
+    def _stage(self, stepper, stage, dt, x, row_lo, row_hi, poison=False):
+        # ssprk33_step (proj/include/hweno/timestep.hpp:54-71), interior only
+        f = self._rhs(x, poison)
         X = from_rows(self.regs[x][HALO:HALO + self.nrho].numpy(), self.nt)
         U = from_rows(self.regs[self.cur][HALO:HALO + self.nrho].numpy(), self.nt)
         if stage == 0:
@@ -94,6 +116,5 @@ class CpuSlab:
             out, dst = 0.75 * U + 0.25 * (X + dt * f), self.scr2
         else:
             out, dst = (1.0 / 3.0) * U + (2.0 / 3.0) * (X + dt * f), self.scr1
-        self.regs[dst][HALO:HALO + self.nrho] = torch.from_numpy(to_rows(out, self.nchunks))
-        if stage == 2:
-            self.cur, self.scr1 = self.scr1, self.cur
+        rows = torch.from_numpy(to_rows(out, self.nchunks))
+        self.regs[dst][HALO + row_lo:HALO + row_hi] = rows[row_lo:row_hi]

@@ -165,6 +165,52 @@ def test_blowup_freezes_state(cuda_ok):
     assert not np.all(np.isfinite(interior(frozen))) or np.max(np.abs(interior(frozen))) > 1e30
 
 
+def test_stage_parts_equal_whole_stages(cuda_ok):
+    """hwg_launch_stage_rows: a stage run as interior rows + two strips (the
+    overlapped halo exchange of SURVEY.md §8e) equals the whole-stage launch
+    bit for bit, for RK3 and RK(10,4); and on a blow-up the deferred
+    publication freezes the state exactly like whole stages do."""
+    for case in ("kerr09_w5", "kerr09_w5_rk104", "extremal_fd6ko"):
+        g = load_golden(case)
+        stepper = str(g["stepper"])
+        ns = 3 if stepper == "ssprk33" else 10
+        h = 4 if str(g["scheme"]) == "fd6ko" else 3
+        dt = (float(g["dt"][0]), float(g["dt"][1]))
+        for mode in ("f64", "mixed"):
+            whole = gpu_from_golden(g, mode)
+            whole.set_state(g["u0"])
+            whole.launch_steps(stepper, dt, 0, 4)
+            parts = gpu_from_golden(g, mode)
+            parts.set_state(g["u0"])
+            n = parts.nrho
+            for q in range(4):
+                for st in range(ns):
+                    parts.launch_stage_rows(stepper, st, dt, q, h, n - h, True, False)
+                    parts.launch_stage_rows(stepper, st, dt, q, 0, h, False, False)
+                    parts.launch_stage_rows(stepper, st, dt, q, n - h, n, False, True)
+            assert np.array_equal(whole.get_state(), parts.get_state()), (case, mode)
+    g = load_golden("extremal_w5")
+    u = g["u0"].copy()
+    u[0, 2 + 1, 4 + 30] = 1e31
+    dt = (float(g["dt"][0]), float(g["dt"][1]))
+    parts = gpu_from_golden(g, "mixed")
+    parts.set_state(u)
+    n = parts.nrho
+    for q in range(3):
+        for st in range(3):
+            parts.launch_stage_rows("ssprk33", st, dt, q, 3, n - 3, True, False)
+            parts.launch_stage_rows("ssprk33", st, dt, q, 0, 3, False, False)
+            parts.launch_stage_rows("ssprk33", st, dt, q, n - 3, n, False, True)
+    blown, step = parts.status()
+    assert blown and step == 1
+    one = gpu_from_golden(g, "mixed")
+    one.set_state(u)
+    one.launch_steps("ssprk33", dt, 0, 1)
+    np.testing.assert_array_equal(interior(parts.get_state()), interior(one.get_state()))
+    with pytest.raises(ValueError):
+        parts.launch_stage_rows("ssprk33", 0, dt, 0, 0, n + 1, True, True)
+
+
 def test_observers_match_reference(cuda_ok):
     import oracle as O
     if not O.ref_available():
@@ -275,7 +321,8 @@ def test_c2_full_size_prefix_vs_reference(cuda_ok):
 
 @pytest.mark.parametrize("case,nslabs", [("kerr09_w5", 2), ("kerr09_w5", 3), ("extremal_w5_theta34", 2),
                                          ("extremal_fd6ko", 2), ("kerr09_w5_rk104", 2)])
-def test_radial_slabs_bit_identical(cuda_ok, case, nslabs):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_radial_slabs_bit_identical(cuda_ok, case, nslabs, overlap):
     """radial slabs with halo exchange reproduce the single-GPU
     result bitwise (the GPU form of criterion 12, acceptance_parallel.cpp).
     Slabs are emulated as handles on one GPU with stream-ordered halo copies."""
@@ -304,7 +351,8 @@ def test_radial_slabs_bit_identical(cuda_ok, case, nslabs):
             u[:, 2:-2, 4:-4] = g["u0"][:, 2:-2, 4 + off:4 + off + cnt]
             h.set_state(u)
             slabs.append((off, cnt, h))
-        LocalSlabs([h for _, _, h in slabs], str(g["scheme"])).steps(stepper, dt, 0, 6)
+        LocalSlabs([h for _, _, h in slabs], str(g["scheme"]), overlap=overlap).steps(
+            stepper, dt, 0, 6)
         torch.cuda.synchronize()
         for off, cnt, h in slabs:
             got = h.get_state()

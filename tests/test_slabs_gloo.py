@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, steps, q):
+def _worker(rank, world, port, case, steps, q, overlap=False):
     sys.path.insert(0, HERE)
     sys.path.insert(0, os.path.dirname(HERE))
     import torch.distributed as dist
@@ -35,14 +35,15 @@ def _worker(rank, world, port, case, steps, q):
     off, cnt = partition(int(g["nrho"]), world)[rank]
     b = CpuSlab(g, off, cnt)
     b.set_interior(g["u0"][:, 2:-2, 4 + off:4 + off + cnt])
-    DistSlab(b, rank, world, str(g["scheme"])).steps("ssprk33", float(g["dt"][0]), 0, steps)
+    DistSlab(b, rank, world, str(g["scheme"]), overlap=overlap).steps(
+        "ssprk33", float(g["dt"][0]), 0, steps)
     q.put((rank, off, b.interior()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_slabs_match_single_domain(world):
+@pytest.mark.parametrize("world,overlap", [(2, False), (3, False), (2, True), (3, True)])
+def test_gloo_slabs_match_single_domain(world, overlap):
     from conftest import load_golden
     from helpers import oracle_from_golden
     case, steps = "kerr09_w5", 4
@@ -50,7 +51,7 @@ def test_gloo_slabs_match_single_domain(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, steps, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, steps, q, overlap))
              for r in range(world)]
     for p in procs:
         p.start()
