@@ -24,9 +24,10 @@
 // Work decomposition: a warp owns one chunk and a contiguous range of rows;
 // each lane owns one theta column and marches along rho with a register
 // window of the stencil rows, so every state value is read from HBM once
-// (plus the halo rows of each range).  Theta neighbours come from warp
-// shuffles (parity-reflected at the poles, evolve.cpp:59-70); the two lanes at
-// each chunk edge fetch the neighbouring chunk's column one row ahead.  Radial
+// (plus the halo rows of each range).  Theta neighbours come from a per-warp
+// shared-memory row (parity-reflected at the poles, evolve.cpp:59-70); the
+// four lanes at the chunk edges fetch the neighbouring chunks' columns one row
+// ahead.  Radial
 // ghosts at the physical ends are synthesised in registers with the
 // reference's cubic recurrence (evolve.cpp:45-57); slab ends read halo rows.
 //
