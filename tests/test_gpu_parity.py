@@ -404,3 +404,37 @@ def test_radial_convergence_order(cuda_ok, scheme, mode, order):
         gpu.close()
     rates = [math.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
     assert min(rates) >= order, (errs, rates)
+
+
+@pytest.mark.parametrize("nrho,ntheta", [(9, 2), (10, 3), (13, 31), (17, 32), (31, 33),
+                                         (64, 65), (9, 96), (200, 1 + 64)])
+@pytest.mark.parametrize("scheme", ["weno5", "weno3", "fd6ko"])
+def test_ragged_shapes_vs_oracle(cuda_ok, nrho, ntheta, scheme):
+    """Ragged and minimal grids (the stencil-support minimum of
+    evolve.cpp:16-17, nθ not a multiple of the 32-column chunk, one column
+    in the last chunk, ranges of 2 rows touching both physical ends): one
+    RHS and 3 SSP-RK3 steps of a random state against the C restatement,
+    both parities."""
+    from oracle import OracleSolver
+    from paper_2010_04760_b200 import synthetic
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
+    prob = synthetic.problem(nrho, ntheta)
+    rng = np.random.default_rng(nrho * 1000 + ntheta)
+    u = np.zeros((4, ntheta + 4, nrho + 8))
+    u[:, 2:-2, 4:-4] = rng.uniform(-1, 1, (4, ntheta, nrho))
+    dt = 0.1 * prob["drho"]
+    for parity in (1, -1):
+        for mode, tol in (("f64", 1e-12), ("mixed", 1e-6)):
+            gpu = GpuEvolution(nrho, ntheta, prob["drho"], prob["dtheta"], parity, prob["coef"],
+                               prob["cotth"], SchemeSpec(scheme, mode))
+            orc = OracleSolver(nrho, ntheta, prob["drho"], prob["dtheta"], parity, prob["coef"],
+                               prob["cotth"], scheme, mode)
+            ug, du = gpu.rhs(u)
+            uo, duo = orc.rhs(u)
+            assert np.array_equal(ug, uo), (mode, parity)
+            assert rel_linf(du, duo) <= tol, (mode, parity, rel_linf(du, duo))
+            gpu.set_state(u)
+            gpu.launch_steps("ssprk33", dt, 0, 3)
+            us, _ = orc.advance(u, dt, 0, 3)
+            assert rel_linf(gpu.get_state(), us) <= tol, (mode, parity)
+            gpu.close()
