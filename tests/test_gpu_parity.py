@@ -438,3 +438,44 @@ def test_ragged_shapes_vs_oracle(cuda_ok, nrho, ntheta, scheme):
             us, _ = orc.advance(u, dt, 0, 3)
             assert rel_linf(gpu.get_state(), us) <= tol, (mode, parity)
             gpu.close()
+
+
+def test_large_grid_64bit_offsets(cuda_ok):
+    """A grid whose coefficient and state offsets pass 2^32 bytes (262144 x 256:
+    4.8 GB of coefficient blocks, 2.1 GB per state register): two steps of the
+    whole grid equal two radial slabs of it bit for bit, compared on the
+    device — an index computed in 32 bits anywhere would break the equality."""
+    import torch
+    from paper_2010_04760_b200 import synthetic
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
+    from paper_2010_04760_b200.slabs import LocalSlabs, partition
+    n, nt = 262144, 256
+    prob = synthetic.problem(n, nt)
+    u0 = synthetic.initial_state(prob)
+    dt = synthetic.select_dt(prob)
+    stream = torch.cuda.current_stream().cuda_stream
+    spec = SchemeSpec("weno5", "mixed")
+    whole = GpuEvolution(n, nt, prob["drho"], prob["dtheta"], prob["parity"], prob["coef"],
+                         prob["cotth"], spec)
+    whole.set_stream(stream)
+    whole.set_state(u0)
+    whole.launch_steps("ssprk33", dt, 0, 2)
+    slabs = []
+    for off, cnt in partition(n, 2):
+        h = GpuEvolution(cnt, nt, prob["drho"], prob["dtheta"], prob["parity"], prob["coef"],
+                         prob["cotth"], spec, rho_offset=off, nrho_global=n, coef_ld=n,
+                         coef_row0=off)
+        h.set_stream(stream)
+        u = np.zeros((4, nt + 4, cnt + 8))
+        u[:, 2:-2, 4:-4] = u0[:, 2:-2, 4 + off:4 + off + cnt]
+        h.set_state(u)
+        slabs.append((off, cnt, h))
+    LocalSlabs([h for _, _, h in slabs], "weno5").steps("ssprk33", dt, 0, 2)
+    torch.cuda.synchronize()
+    assert not whole.status()[0]
+    W = whole.register_view(whole.current_register())
+    for off, cnt, h in slabs:
+        S = h.register_view(h.current_register())
+        assert torch.equal(S[4:4 + cnt], W[4 + off:4 + off + cnt]), off
+        h.close()
+    whole.close()
