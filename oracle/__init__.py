@@ -58,6 +58,9 @@ def ref_lib():
         lib.ref_create.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int, C.c_double,
                                    C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                    C.c_double, C.c_int, C.POINTER(C.c_void_p)]
+        lib.ref_create_deeper.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int, C.c_double,
+                                          C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                          C.c_double, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
         lib.ref_destroy.argtypes = [C.c_void_p]
         lib.ref_info.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_longlong)]
         lib.ref_coeffs.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp]
@@ -149,12 +152,14 @@ class RefSolver:
     """The reference library: grid + coefficients + EvolutionRhs + advance_steps."""
 
     def __init__(self, phys: Physics, nrho: int, ntheta: int, scheme="weno5", mode="full",
-                 eps=1e-6, sigma=0.01, workers=1):
+                 eps=1e-6, sigma=0.01, workers=1, deeper=0):
+        """deeper > 0: excision `deeper` cells below the default grid of
+        nrho - deeper points, same spacing (test_evolve.cpp:397-410)."""
         lib = ref_lib()
         h = C.c_void_p()
-        _chk(lib.ref_create(phys.M, phys.a, phys.spin, phys.mmode, phys.S, nrho, ntheta,
-                            SCHEMES[scheme], 0 if mode == "full" else 1, eps, sigma,
-                            workers, C.byref(h)))
+        _chk(lib.ref_create_deeper(phys.M, phys.a, phys.spin, phys.mmode, phys.S, nrho, ntheta,
+                                   SCHEMES[scheme], 0 if mode == "full" else 1, eps, sigma,
+                                   workers, deeper, C.byref(h)))
         self.h = h
         self.phys, self.nrho, self.ntheta = phys, nrho, ntheta
         self.scheme, self.mode, self.eps, self.sigma = scheme, mode, eps, sigma

@@ -77,9 +77,23 @@ const char* ref_last_error(void) { return g_err.c_str(); }
 
 // scheme: 0 weno5, 1 weno3, 2 fd6ko; mode: 0 full (DD weights), 1 mixed
 // (fp64 weights).  eps may be +inf (frozen linear weights).
+// deeper > 0: the excision sits `deeper` cells below the default grid of
+// nrho - deeper points, same spacing (make_grid's rho_min overload, as in
+// proj/tests/test_evolve.cpp:397-410)
+int ref_create_deeper(double M, double a, int spin, int mmode, double S, int nrho,
+                      int ntheta, int scheme, int mode, double eps, double sigma,
+                      int workers, int deeper, void** out);
+
 int ref_create(double M, double a, int spin, int mmode, double S, int nrho,
                int ntheta, int scheme, int mode, double eps, double sigma,
                int workers, void** out) {
+  return ref_create_deeper(M, a, spin, mmode, S, nrho, ntheta, scheme, mode, eps, sigma,
+                           workers, 0, out);
+}
+
+int ref_create_deeper(double M, double a, int spin, int mmode, double S, int nrho,
+                      int ntheta, int scheme, int mode, double eps, double sigma,
+                      int workers, int deeper, void** out) {
   *out = nullptr;
   return guarded([&] {
     auto h = std::make_unique<RefHandle>();
@@ -88,7 +102,12 @@ int ref_create(double M, double a, int spin, int mmode, double S, int nrho,
     h->p.spin = spin;
     h->p.mmode = mmode;
     h->p.S = WorkReal(S);
-    h->g = make_grid(nrho, ntheta, h->p);
+    if (deeper > 0) {
+      const Grid g0 = make_grid(nrho - deeper, ntheta, h->p);
+      h->g = make_grid(nrho, ntheta, h->p, g0.rho_min - WorkReal(double(deeper)) * g0.drho);
+    } else {
+      h->g = make_grid(nrho, ntheta, h->p);
+    }
     h->cs = assemble_coefficients(h->g, h->p);
     h->spec.scheme = scheme == 0 ? Scheme::weno5
                      : scheme == 1 ? Scheme::weno3
