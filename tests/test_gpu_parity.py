@@ -584,3 +584,42 @@ def test_pulse_exits_without_reflection(cuda_ok, mode):
         worst = max(worst, float(d.max()))
     assert a_inc[0] >= 0.005, a_inc
     assert worst <= 1e-8 * a_inc[0], (worst, a_inc)
+
+
+def test_rk_amplification_polynomials(cuda_ok):
+    """test_timestep.cpp:68-93 through the fused kernels: with only the
+    C plane set, a spatially uniform state sees F(u) = A u pointwise
+    (A = [[0, 1], [C, 0]] on (Psi, pi); every radial / theta difference of a
+    constant is exactly 0), so one SSP-RK(3,3) step is the cubic Taylor
+    polynomial of dt A, and SSP-RK(10,4) matches exp(dt A) through 4th order."""
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
+    n, nt = 16, 4
+    dth = math.pi / nt
+    cot = 1.0 / np.tan(dth * (np.arange(nt) + 0.5))
+
+    def one_step(C, dt, stepper, mode):
+        coef = np.zeros((9, nt, n))
+        coef[6] = C
+        g = GpuEvolution(n, nt, 0.05, dth, 1, coef, cot, SchemeSpec("weno5", mode))
+        u = np.zeros(g.shape)
+        u[0, 2:-2, 4:-4] = 1.0
+        g.set_state(u)
+        g.launch_steps(stepper, dt, 0, 1)
+        v = g.get_state()
+        g.close()
+        return v[0, 2:-2, 4:-4], v[2, 2:-2, 4:-4]
+
+    for mode in ("f64", "mixed"):
+        for C in (1.0, 0.25, -0.3):
+            for dt in (0.1, 0.01, 0.7):
+                M = dt * np.array([[0.0, 1.0], [C, 0.0]])
+                P = np.eye(2) + M + M @ M / 2 + M @ M @ M / 6
+                psi, pi = one_step(C, dt, "ssprk33", mode)
+                assert np.max(np.abs(psi - P[0, 0])) <= 1e-14
+                assert np.max(np.abs(pi - P[1, 0])) <= 1e-14
+        diffs = []
+        for dt in (0.4, 0.2, 0.1, 0.05):
+            psi, pi = one_step(1.0, dt, "ssprk104", mode)
+            diffs.append(max(np.max(np.abs(psi - math.cosh(dt))), np.max(np.abs(pi - math.sinh(dt)))))
+        slopes = [math.log2(diffs[i] / diffs[i + 1]) for i in range(3)]
+        assert min(slopes) >= 4.5 and diffs[-1] <= 1e-7, (diffs, slopes)
