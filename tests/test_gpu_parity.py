@@ -623,3 +623,39 @@ def test_rk_amplification_polynomials(cuda_ok):
             diffs.append(max(np.max(np.abs(psi - math.cosh(dt))), np.max(np.abs(pi - math.sinh(dt)))))
         slopes = [math.log2(diffs[i] / diffs[i + 1]) for i in range(3)]
         assert min(slopes) >= 4.5 and diffs[-1] <= 1e-7, (diffs, slopes)
+
+
+@pytest.mark.parametrize("scheme,mode,order", [("weno5", "f64", 4.5), ("weno5", "mixed", 4.5),
+                                               ("fd6ko", "f64", 5.5)])
+def test_mms_residual_order(cuda_ok, scheme, mode, order):
+    """Criterion 6 (acceptance_mms.cpp, harness.cpp:120-185): four
+    theta-independent Gaussian bumps on the extremal-Kerr s=-2 grid with the
+    reference's coefficient planes; the GPU RHS against the analytic RHS
+    built from the same planes (pure radial truncation error), least-squares
+    order over {128, 192, 256, 384} x 8."""
+    import oracle as O
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
+    bumps = ((8.5, 0.80, 1.00), (10.0, 0.90, 0.70), (11.5, 0.85, -0.60), (9.2, 1.00, 0.45))
+    ns, errs = (128, 192, 256, 384), []
+    for n in ns:
+        ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=0), n, 8, scheme=scheme)
+        rho = ref.rho
+        val = [a * np.exp(-((rho - c) ** 2) / (2 * w * w)) for c, w, a in bumps]
+        der = [-((rho - c) / (w * w)) * v for (c, w, a), v in zip(bumps, val)]
+        cf = ref.coef.reshape(9, 8, n)
+        b, lam, wr, wi, btr, bti, cr, ci = cf[:8]
+        ex = np.stack([val[2] - b * der[0], val[3] - b * der[1],
+                       -lam * der[2] + wr * der[0] - wi * der[1] + btr * val[2] - bti * val[3]
+                       + cr * val[0] - ci * val[1],
+                       -lam * der[3] + wr * der[1] + wi * der[0] + btr * val[3] + bti * val[2]
+                       + cr * val[1] + ci * val[0]])
+        gpu = GpuEvolution.from_reference(ref, SchemeSpec(scheme, mode, 1e-6, 0.01))
+        u = np.zeros(gpu.shape)
+        for c in range(4):
+            u[c, 2:-2, 4:-4] = val[c][None, :]
+        _, du = gpu.rhs(u)
+        errs.append(float(np.max(np.abs(du[:, 2:-2, 4:-4] - ex))))
+        gpu.close()
+    x, y = np.log(ns), np.log(errs)
+    fit = -np.polyfit(x, y, 1)[0]
+    assert fit >= order and all(errs[i + 1] < errs[i] for i in range(3)), (errs, fit)
