@@ -292,27 +292,29 @@ def test_c2_full_size_prefix_vs_reference(cuda_ok):
     """BASELINE configs[1] at its full size (extremal Kerr s=-2 m=2,
     4096x128), the reference library run live on the box's cores for a
     prefix of the evolution: GPU mixed vs reference mixed <= 1e-6, GPU f64 vs
-    reference full <= 1e-12, and the dd-mixed tier bit for bit."""
+    reference full <= 1e-12, and the dd-mixed tier bit for bit — with SSP-RK3
+    and with the production stepper SSP-RK(10,4)."""
     import oracle as O
     from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
     phys = O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22)
     cores = os.cpu_count() or 1
-    for mode, K in (("mixed", 20), ("full", 10)):
+    for mode, K, stepper in (("mixed", 20, "ssprk33"), ("full", 10, "ssprk33"),
+                             ("mixed", 4, "ssprk104")):
         ref = O.RefSolver(phys, 4096, 128, mode=mode, workers=cores)
         (hi, lo) = ref.initial_data()
-        dt = ref.select_dt()
-        (rh, rl), st, _ = ref.advance(hi, lo, dt, 0, K)
+        dt = ref.select_dt(stepper)
+        (rh, rl), st, _ = ref.advance(hi, lo, dt, 0, K, stepper=stepper)
         assert st["steps_done"] == K and not st["blew_up"]
         gpu = GpuEvolution.from_reference(ref)
         gpu.set_state(hi)
-        gpu.advance("ssprk33", dt, 0, K)
+        gpu.advance(stepper, dt, 0, K)
         err = rel_linf(gpu.get_state(), rh)
         assert err <= (1e-6 if mode == "mixed" else 1e-12), (mode, err)
         gpu.close()
         if mode == "mixed":
             dd = GpuEvolution.from_reference(ref, SchemeSpec("weno5", "dd-mixed", ref.eps))
             dd.set_state(hi, lo)
-            dd.advance("ssprk33", dt, 0, K)
+            dd.advance(stepper, dt, 0, K)
             gh, gl = dd.get_state_dd()
             assert np.array_equal(interior(gh).view(np.uint64), interior(rh).view(np.uint64))
             assert np.array_equal(interior(gl).view(np.uint64), interior(rl).view(np.uint64))
