@@ -38,6 +38,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>  // device printf of the HWG_DEBUG bounds checks
 
 #ifndef HWG_MINB
 // resident blocks per SM: 3 (12 warps at up to 168 registers, room for the
@@ -125,6 +126,30 @@ struct StageArgs {
 };
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
+
+// Debug builds (-DHWG_DEBUG, tools/build_variant.sh dbg -DHWG_DEBUG): every
+// global address the stage kernel forms is checked against the extent of the
+// array it points into, trapping on a violation (compute-sanitizer is not
+// available on the GPU pool; the GPU test suite runs against this build).
+#ifdef HWG_DEBUG
+#define HWG_CHK(cond)                                                                    \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("hwg bounds check failed: %s (line %d, block %d, thread %d)\n", #cond,      \
+             __LINE__, blockIdx.x, threadIdx.x);                                         \
+      asm volatile("trap;");                                                             \
+    }                                                                                    \
+  } while (0)
+#else
+#define HWG_CHK(cond) \
+  do {                \
+  } while (0)
+#endif
+// p .. p + len (double2) inside a state register given by its row-0 pointer
+__device__ __forceinline__ bool in_reg(const double2* p, const double2* row0, ptrdiff_t rs, int n,
+                                       int len) {
+  return p >= row0 - kHalo * rs && p + len <= row0 + (ptrdiff_t)(n + kHalo) * rs;
+}
 __device__ __forceinline__ double2 neg2(double2 v) { return make_double2(-v.x, -v.y); }
 
 // reference cubic continuation p[-t] = 4p[-t+1] - 6p[-t+2] + 4p[-t+3] - p[-t+4]
@@ -574,6 +599,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
   // lane 0: the copies of iteration j into slot s.  The coefficient block
   // does not depend on the previous stage; the state blocks do.
   auto issue_coef = [&](int s, int j) {  // before pdl_wait: bytes expected, no arrival
+    HWG_CHK(j >= 0 && j < n && chunk < a.nchunks);
     const uint32_t bar = bar0 + s * 8;
     mbar_expect_tx_only(bar, kCoefBlk * 16);
     bulk_g2s(smem_u32(ring + (size_t)s * SB) + SlotT::COEF, cblk + j * crs, kCoefBlk * 16, bar);
@@ -586,6 +612,11 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
     const uint32_t bytes =
         SlotT::BYTES - (st ? 0 : kStateBlk * 16) - (with_coef ? 0 : kCoefBlk * 16);
     mbar_expect_tx(bar, bytes);  // + the arrival that completes the phase
+    HWG_CHK(j >= 0 && j < n);
+    HWG_CHK(!st || in_reg(xblk + rn * rs, a.x, rs, n, kStateBlk));
+    HWG_CHK(!SlotT::HAS_A || in_reg(a.ua + j * rs + chunk * kStateBlk, a.ua, rs, n, kStateBlk));
+    HWG_CHK(!SlotT::HAS_BG || (in_reg(a.ub + j * rs + chunk * kStateBlk, a.ub, rs, n, kStateBlk) &&
+                               in_reg(a.ug + j * rs + chunk * kStateBlk, a.ug, rs, n, kStateBlk)));
     if (with_coef) bulk_g2s(dst + SlotT::COEF, cblk + j * crs, kCoefBlk * 16, bar);
     if (st) bulk_g2s(dst + SlotT::XN, xblk + rn * rs, kStateBlk * 16, bar);
     const ptrdiff_t o = j * rs + chunk * kStateBlk;
@@ -640,6 +671,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
   if (lo_ghosts) {
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
+      HWG_CHK(in_reg(xps + m * rs, a.x, rs, n, 1) && in_reg(xpi + m * rs, a.x, rs, n, 1));
       gs[IL + m] = __ldcg(xps + m * rs);
       gp[IL + m] = __ldcg(xpi + m * rs);
     }
@@ -659,6 +691,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
       ips[m] = cubic(ips[m - 1], ips[m - 2], ips[m - 3], ips[m - 4]);
       ipi[m] = cubic(ipi[m - 1], ipi[m - 2], ipi[m - 3], ipi[m - 4]);
     } else {
+      HWG_CHK(in_reg(xps + r * rs, a.x, rs, n, 1) && in_reg(xpi + r * rs, a.x, rs, n, 1));
       ips[m] = __ldcg(xps + r * rs);
       ipi[m] = __ldcg(xpi + r * rs);
     }
@@ -681,6 +714,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
   bool bad = false;
   // theta halo, software-pipelined one row ahead (4 lanes)
   const double2* hrow = a.x + hoff + (ptrdiff_t)jb * rs;
+  HWG_CHK(!has_h || in_reg(hrow, a.x, rs, n, 1));
   double2 hn = has_h ? ld2(hrow) : make_double2(0.0, 0.0);
   int slot = 0;
   uint32_t parity = 0;
@@ -697,6 +731,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
     const double2* sd = reinterpret_cast<const double2*>(sl) + lane;
     double2 h = hflip ? neg2(hn) : hn;
     hrow += rs;
+    HWG_CHK(!(has_h && j + 1 < je) || in_reg(hrow, a.x, rs, n, 1));
     if (has_h && j + 1 < je) hn = ld2(hrow);
     mbar_wait(bar0 + slot * 8, parity);
     const double2 bl = sd[0];
@@ -716,6 +751,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
         if (!o && SCH == WENO5) {
           // plus at j - 1/2 needs row j - 3, outside the window
           double2 xx[PW + 1];
+          HWG_CHK(j - 3 >= -kHalo);
           xx[0] = row_or_ghost(xpi, j - 3, rs, a.phys_lo);
 #pragma unroll
           for (int m = 0; m < PW; ++m) xx[m + 1] = wpi[m];
@@ -752,6 +788,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
                                  __shfl_sync(kFull, ps.y, wsrc & 31));
       // image column in the previous chunk (last chunk with one column)
       if (!active && (wsrc < 0 || wsrc > 31))
+        HWG_CHK(in_reg(a.x + (ptrdiff_t)j * rs + psi_off(k0 + wsrc), a.x, rs, n, 1));
         img = ld2(a.x + (ptrdiff_t)j * rs + psi_off(k0 + wsrc));
       if (!active) wv = wflip ? neg2(img) : img;
     }
@@ -831,10 +868,12 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
     }
     if (active) {
       double2* ob = a.o + j * rs + chunk * kStateBlk + lane;
+      HWG_CHK(j >= 0 && j < n && in_reg(ob, a.o, rs, n, 33));
       ob[0] = ops;
       ob[32] = opv;
       if (EPI == EPI_RK104_5) {
         double2* fb = a.f + j * rs + chunk * kStateBlk + lane;
+        HWG_CHK(in_reg(fb, a.f, rs, n, 33));
         fb[0] = make_double2(f0, f1);
         fb[32] = make_double2(f2v, f3);
       }
