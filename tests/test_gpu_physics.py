@@ -161,3 +161,37 @@ def test_crit8_scheme_ranking_mixed_tier(cuda_ok):
                 assert abs(dg[n] - dr[n]) <= 0.01 * max(dr[n], 0.01), n
         have = [n for n in dr if dr[n] is not None]
         assert sorted(have, key=lambda n: dr[n]) == sorted(have, key=lambda n: dg[n])
+
+
+def test_kerr09_desk_tail(cuda_ok):
+    """BASELINE configs[2] physics (Kerr a = 0.9, s = -2, l = 2 pulse) at the
+    desk scale SURVEY.md D7 prescribes for the tail-exponent parity (2048x32,
+    SSP-RK(10,4), tau to 500; the full 16384x128, 10^6-step run is GPU-only,
+    tests/production_c3.py).  The reference-precision tier reproduces the
+    reference run exactly (observer series, window indices to ~1e-9), the
+    late-time exponents included."""
+    import oracle as O
+    from paper_2010_04760_b200.hwgpu import SchemeSpec
+    fx = _fixture("kerr09_desk")
+    init = O.Physics(a=0.9, spin=-2, mmode=0, ell=2, center=3.0, width=0.3)
+    ref = O.RefSolver(init, 2048, 32, scheme="weno5", mode="mixed")
+    rows, st = tails.gpu_run_series(ref, init, SchemeSpec("weno5", "dd-mixed"), "ssprk104",
+                                    tau_end=500.0)
+    assert not st["blew_up"] and st["steps_done"] == int(fx["planned"])
+    w = tuple(fx["window"])
+    g = tails.summary(rows, w)
+    r = tails.summary(fx["rows"], w)
+    print("gpu", g, "\nref", r)
+    np.testing.assert_array_equal(rows[:, 0], fx["rows"][:, 0])
+    for k in ("p_phi", "p_dphi", "p_proj", "charge"):
+        assert abs(g[k] - r[k]) <= 1e-9 * max(abs(r[k]), 1.0), k
+        assert _rel(g[k], r[k]) <= 0.01, k
+    # the fp64 tier follows the reference while the horizon field is well
+    # above its rounding floor (tau in [100, 200], |d_rho Phi| ~ 4e-5); by
+    # tau ~ 300 (|d_rho Phi| ~ 1e-11) only the extended-precision state does
+    rows64, _ = tails.gpu_run_series(ref, init, SchemeSpec("weno5", "f64"), "ssprk104",
+                                     tau_end=500.0)
+    early = (100.0, 200.0)
+    g64, r64 = tails.summary(rows64, early), tails.summary(fx["rows"], early)
+    for k in ("p_phi", "p_proj", "charge"):
+        assert _rel(g64[k], r64[k]) <= 0.01, (k, g64[k], r64[k])

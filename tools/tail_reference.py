@@ -35,6 +35,11 @@ RUNS = {
     "price_schw": dict(phys=Physics(a=0.0, spin=0, mmode=0, ell=2, center=3.0, width=0.3),
                        nrho=1024, ntheta=16, scheme="weno5", mode="mixed", stepper="ssprk104",
                        tau_end=800.0, window=(500.0, 750.0)),
+    # BASELINE configs[2] physics (Kerr a = 0.9, s = -2, l = 2 pulse; SURVEY.md
+    # D5/D7) at the desk scale D7 prescribes for the tail-exponent parity
+    "kerr09_desk": dict(phys=Physics(a=0.9, spin=-2, mmode=0, ell=2, center=3.0, width=0.3),
+                        nrho=2048, ntheta=32, scheme="weno5", mode="mixed", stepper="ssprk104",
+                        tau_end=500.0, window=(300.0, 500.0)),
 }
 
 
