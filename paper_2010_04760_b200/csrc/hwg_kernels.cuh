@@ -540,13 +540,32 @@ static __device__ __noinline__ void launch_ticket(unsigned long long* tick,
   }
 }
 
-template <int SCH, int MODE, int EPI>
-__device__ __forceinline__ bool stage_body(const StageArgs& a);
+template <int SCH, int MODE, int EPI, class WaitIn>
+__device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ring, uint32_t bar0,
+                                           double2* trow, WaitIn&& wait_in);
+
+// shared memory of one warp for a whole-launch stage: its ring, its ring's
+// mbarriers, its theta row (stage_smem_bytes)
+template <int EPI>
+__device__ __forceinline__ void stage_layout(unsigned char*& ring, uint32_t& bar0,
+                                             double2*& trow) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int S = Slot<EPI>::S, SB = Slot<EPI>::BYTES;
+  const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  ring = smem + (size_t)wib * S * SB;
+  bar0 = smem_u32(smem + (size_t)wpb * S * SB) + wib * S * 8;
+  trow = reinterpret_cast<double2*>(smem + stage_theta_offset<EPI>(wpb)) + wib * 36;
+}
 
 template <int SCH, int MODE, int EPI>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_MINB)
 stage_kernel(const StageArgs a) {
-  if (!stage_body<SCH, MODE, EPI>(a)) return;  // frozen
+  unsigned char* ring;
+  uint32_t bar0;
+  double2* trow;
+  stage_layout<EPI>(ring, bar0, trow);
+  // the previous stage's grid has completed; its writes are visible
+  if (!stage_body<SCH, MODE, EPI>(a, ring, bar0, trow, [] { pdl_wait(); })) return;  // frozen
   // let the next stage's grid launch once this warp's rows are done (measured:
   // triggering at kernel start lets the next grid's waiting blocks take SM
   // slots early and costs 12 % at C5; triggering here gains 3-5 % on the
@@ -556,9 +575,107 @@ stage_kernel(const StageArgs a) {
     launch_ticket(a.tick, a.flag, (a.px.on_lo | a.px.on_hi) ? a.px.epoch : nullptr);
 }
 
-// false: the state is frozen (an earlier step blew up) and nothing was done
-template <int SCH, int MODE, int EPI>
-__device__ __forceinline__ bool stage_body(const StageArgs& a) {
+// ---------------------------------------------------------------------------
+// Step kernel (opt-in, single GPU, SSP-RK3 fast tiers): the three stages of
+// one step in ONE cooperative launch.  Between stages a warp waits only for
+// its four dataflow neighbours — ranges r-1, r+1 of its chunk (radial halo
+// rows) and chunks c-1, c+1 of its range (theta halo columns, pole images) —
+// to have finished the previous stage, which covers both the read-after-write
+// of the stage inputs and the write-after-read of the register a stage
+// overwrites.  Saves the launch / ramp / tail of two of the three stages on
+// launch-bound grids.  prog[] counts the stages each warp has completed
+// (monotonic across launches, equal for all warps between launches).
+struct StepArgs {
+  StageArgs st[3];
+  unsigned long long* prog;        // per warp (range * nchunks + chunk)
+  long long timeout_ns;            // bounded neighbour wait: flag[0] |= 4 on expiry
+};
+
+__host__ __device__ constexpr size_t step_bar_offset(int wpb) {
+  return (size_t)wpb * Slot<EPI_RK3>::S * Slot<EPI_RK3>::BYTES;
+}
+__host__ __device__ constexpr size_t step_theta_offset(int wpb) {
+  return (step_bar_offset(wpb) + (size_t)3 * wpb * Slot<EPI_RK3>::S * 8 + 15) & ~(size_t)15;
+}
+constexpr size_t step_smem_bytes(int wpb = kWarpsPerBlock) {
+  return step_theta_offset(wpb) + (size_t)wpb * 36 * 16;
+}
+
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int SCH, int MODE, int EPI, class WaitIn>
+__device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ring, uint32_t bar0,
+                                           double2* trow, WaitIn&& wait_in);
+
+template <int SCH, int MODE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_MINB)
+step_kernel(const StepArgs sa) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int S = Slot<EPI_RK3>::S, SB = Slot<EPI_RK3>::BYTES;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const StageArgs& a0 = sa.st[0];
+  const int gw = blockIdx.x * wpb + wib;
+  const int nch = a0.nchunks;
+  const int chunk = gw % nch, range = gw / nch;
+  const bool live = range < a0.nranges;
+  unsigned char* ring = smem + (size_t)wib * S * SB;
+  const uint32_t bars = smem_u32(smem + step_bar_offset(wpb));
+  double2* trow = reinterpret_cast<double2*>(smem + step_theta_offset(wpb)) + wib * 36;
+  unsigned long long base = 0;
+  if (live && lane == 0) base = *(volatile unsigned long long*)(sa.prog + gw);
+  base = __shfl_sync(kFull, base, 0);
+  auto wait_nb = [&](int st) {
+    if (live && lane == 0) {
+      const unsigned long long want = base + (unsigned long long)st;
+      const int nb[4] = {range > 0 ? gw - nch : -1, range + 1 < a0.nranges ? gw + nch : -1,
+                         chunk > 0 ? gw - 1 : -1, chunk + 1 < nch ? gw + 1 : -1};
+      bool ok = true;
+      for (int i = 0; i < 4; ++i) {
+        if (nb[i] < 0) continue;
+        const unsigned long long* p = sa.prog + nb[i];
+        if (ld_acquire_gpu(p) >= want) continue;
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_gpu(p) < want) {
+          __nanosleep(64);
+          if ((long long)(globaltimer() - t0) > sa.timeout_ns) { ok = false; break; }
+        }
+      }
+      if (!ok) atomicOr(a0.flag, 4ull);
+      // the inputs arrive through the bulk-copy (async) proxy
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncwarp();
+  };
+  auto publish = [&](int st) {
+    __syncwarp();
+    if (live && lane == 0) {
+      __threadfence();
+      st_release_gpu(sa.prog + gw, base + (unsigned long long)st + 1ull);
+    }
+  };
+  auto bar = [&](int st) { return bars + (uint32_t)((st * wpb + wib) * S * 8); };
+  if (!stage_body<SCH, MODE, EPI_AXPY>(sa.st[0], ring, bar(0), trow, [] {})) return;  // frozen
+  publish(0);
+  stage_body<SCH, MODE, EPI_RK3>(sa.st[1], ring, bar(1), trow, [&] { wait_nb(1); });
+  publish(1);
+  stage_body<SCH, MODE, EPI_RK3C>(sa.st[2], ring, bar(2), trow, [&] { wait_nb(2); });
+  publish(2);
+  if (sa.st[2].tick != nullptr) launch_ticket(sa.st[2].tick, sa.st[2].flag, nullptr);
+}
+
+// false: the state is frozen (an earlier step blew up) and nothing was done.
+// ring / bar0 / trow: this warp's shared memory; wait_in(): returns once the
+// stage's inputs written by other warps or grids are visible.
+template <int SCH, int MODE, int EPI, class WaitIn>
+__device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ring, uint32_t bar0,
+                                           double2* trow, WaitIn&& wait_in) {
   using Wn = Win<SCH>;
   using SlotT = Slot<EPI>;
   constexpr int SL = Wn::SL, PL = Wn::PL, R = Wn::R, SW = Wn::SW, PW = Wn::PW;
@@ -591,8 +708,6 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
   bool wflip;
   const int wsrc = reflect_col(k, nt, wflip, a.negpar) - k0;
 
-  unsigned char* ring = smem + (size_t)wib * S * SB;
-  const uint32_t bar0 = smem_u32(smem + (size_t)wpb * S * SB) + wib * S * 8;
   const double2* xblk = a.x + chunk * kStateBlk;         // this chunk's block at row 0
   const double2* cblk = a.coef + chunk * kCoefBlk;
 
@@ -631,9 +746,11 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
   if (lane == 0 && live) {
     for (int s = 0; s < S; ++s) mbar_init(bar0 + s * 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the ring may have been read by an earlier stage of the same launch
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (int q = 0; q < nq; ++q) issue_coef(q, jb + q);
   }
-  pdl_wait();  // the previous stage's grid has completed; its writes are visible
+  wait_in();
   if (a.flag != nullptr && *(volatile unsigned long long*)a.flag != 0ull) {  // frozen
     if (lane == 0)
       for (int q = 0; q < nq; ++q) {  // drain the coefficient copies before exiting
@@ -794,7 +911,6 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a) {
     }
     // the chunk's extended row E[i] = Psi(k0 - 2 + i), i < 36, in shared memory
     // (one store + four loads instead of 12 double shuffles and selects)
-    double2* trow = reinterpret_cast<double2*>(smem + stage_theta_offset<EPI>(wpb)) + wib * 36;
     trow[lane + 2] = wv;
     if (lane < 2) trow[lane] = h;
     else if (lane >= 30) trow[lane + 4] = h;

@@ -12,7 +12,9 @@ def main():
     from paper_2010_04760_b200 import hwgpu, synthetic
     out = sys.argv[1]
     mode = sys.argv[2] if len(sys.argv) > 2 else "mixed"
-    n, nt, K = 4096, 128, 20
+    n = int(sys.argv[3]) if len(sys.argv) > 3 else 4096
+    nt = int(sys.argv[4]) if len(sys.argv) > 4 else 128
+    K = 20
     prob = synthetic.problem(n, nt)
     g = hwgpu.GpuEvolution(n, nt, prob["drho"], prob["dtheta"], prob["parity"], prob["coef"],
                            prob["cotth"], hwgpu.SchemeSpec("weno5", mode))
