@@ -575,101 +575,6 @@ stage_kernel(const StageArgs a) {
     launch_ticket(a.tick, a.flag, (a.px.on_lo | a.px.on_hi) ? a.px.epoch : nullptr);
 }
 
-// ---------------------------------------------------------------------------
-// Step kernel (opt-in, single GPU, SSP-RK3 fast tiers): the three stages of
-// one step in ONE cooperative launch.  Between stages a warp waits only for
-// its four dataflow neighbours — ranges r-1, r+1 of its chunk (radial halo
-// rows) and chunks c-1, c+1 of its range (theta halo columns, pole images) —
-// to have finished the previous stage, which covers both the read-after-write
-// of the stage inputs and the write-after-read of the register a stage
-// overwrites.  Saves the launch / ramp / tail of two of the three stages on
-// launch-bound grids.  prog[] counts the stages each warp has completed
-// (monotonic across launches, equal for all warps between launches).
-struct StepArgs {
-  StageArgs st[3];
-  unsigned long long* prog;        // per warp (range * nchunks + chunk)
-  long long timeout_ns;            // bounded neighbour wait: flag[0] |= 4 on expiry
-};
-
-__host__ __device__ constexpr size_t step_bar_offset(int wpb) {
-  return (size_t)wpb * Slot<EPI_RK3>::S * Slot<EPI_RK3>::BYTES;
-}
-__host__ __device__ constexpr size_t step_theta_offset(int wpb) {
-  return (step_bar_offset(wpb) + (size_t)3 * wpb * Slot<EPI_RK3>::S * 8 + 15) & ~(size_t)15;
-}
-constexpr size_t step_smem_bytes(int wpb = kWarpsPerBlock) {
-  return step_theta_offset(wpb) + (size_t)wpb * 36 * 16;
-}
-
-__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int SCH, int MODE, int EPI, class WaitIn>
-__device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ring, uint32_t bar0,
-                                           double2* trow, WaitIn&& wait_in);
-
-template <int SCH, int MODE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_MINB)
-step_kernel(const StepArgs sa) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int S = Slot<EPI_RK3>::S, SB = Slot<EPI_RK3>::BYTES;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  const StageArgs& a0 = sa.st[0];
-  const int gw = blockIdx.x * wpb + wib;
-  const int nch = a0.nchunks;
-  const int chunk = gw % nch, range = gw / nch;
-  const bool live = range < a0.nranges;
-  unsigned char* ring = smem + (size_t)wib * S * SB;
-  const uint32_t bars = smem_u32(smem + step_bar_offset(wpb));
-  double2* trow = reinterpret_cast<double2*>(smem + step_theta_offset(wpb)) + wib * 36;
-  unsigned long long base = 0;
-  if (live && lane == 0) base = *(volatile unsigned long long*)(sa.prog + gw);
-  base = __shfl_sync(kFull, base, 0);
-  auto wait_nb = [&](int st) {
-    if (live && lane == 0) {
-      const unsigned long long want = base + (unsigned long long)st;
-      const int nb[4] = {range > 0 ? gw - nch : -1, range + 1 < a0.nranges ? gw + nch : -1,
-                         chunk > 0 ? gw - 1 : -1, chunk + 1 < nch ? gw + 1 : -1};
-      bool ok = true;
-      for (int i = 0; i < 4; ++i) {
-        if (nb[i] < 0) continue;
-        const unsigned long long* p = sa.prog + nb[i];
-        if (ld_acquire_gpu(p) >= want) continue;
-        const unsigned long long t0 = globaltimer();
-        while (ld_acquire_gpu(p) < want) {
-          __nanosleep(64);
-          if ((long long)(globaltimer() - t0) > sa.timeout_ns) { ok = false; break; }
-        }
-      }
-      if (!ok) atomicOr(a0.flag, 4ull);
-      // the inputs arrive through the bulk-copy (async) proxy
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncwarp();
-  };
-  auto publish = [&](int st) {
-    __syncwarp();
-    if (live && lane == 0) {
-      __threadfence();
-      st_release_gpu(sa.prog + gw, base + (unsigned long long)st + 1ull);
-    }
-  };
-  auto bar = [&](int st) { return bars + (uint32_t)((st * wpb + wib) * S * 8); };
-  if (!stage_body<SCH, MODE, EPI_AXPY>(sa.st[0], ring, bar(0), trow, [] {})) return;  // frozen
-  publish(0);
-  stage_body<SCH, MODE, EPI_RK3>(sa.st[1], ring, bar(1), trow, [&] { wait_nb(1); });
-  publish(1);
-  stage_body<SCH, MODE, EPI_RK3C>(sa.st[2], ring, bar(2), trow, [&] { wait_nb(2); });
-  publish(2);
-  if (sa.st[2].tick != nullptr) launch_ticket(sa.st[2].tick, sa.st[2].flag, nullptr);
-}
-
 // false: the state is frozen (an earlier step blew up) and nothing was done.
 // ring / bar0 / trow: this warp's shared memory; wait_in(): returns once the
 // stage's inputs written by other warps or grids are visible.

@@ -14,10 +14,6 @@ void launch_stage_fast(const StageArgs& a, int scheme, int mode, int epi, int bl
 // sets every kernel's smem attribute
 cudaError_t occupancy_fast(int* blocks_per_sm, int mode);
 void init_attributes_fast();
-// the step kernel (three SSP-RK3 stages in one cooperative launch), WENO5 fp64 /
-// mixed; cudaErrorNotSupported otherwise
-cudaError_t launch_step_fast(const StepArgs& a, int scheme, int mode, int blocks, int wpb,
-                             cudaStream_t stream);
 // double-double tiers (stage_kernel_dd)
 void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks, int wpb,
                      cudaStream_t stream);

@@ -140,8 +140,6 @@ struct hwg_solver {
   bool use_graphs = true;
   bool use_pdl = true;       // programmatic dependent launch of the stage kernels
   bool abort_req = false;    // hwg_abort_advance called from the hook
-  bool use_step = false;     // HWG_STEP_KERNEL=1: three RK3 stages per cooperative launch
-  unsigned long long* prog = nullptr;  // step kernel: stages completed per warp
   // observers
   int kobs = -1, j0 = -1, jobs = -1;
   double* obs_w = nullptr;   // 32 horizon weights + ntheta projection weights
@@ -570,39 +568,6 @@ int do_stage_part(hwg_solver* s, int stepper, int stage, double dt_hi, double dt
   return rc;
 }
 
-// One SSP-RK3 step as ONE cooperative launch of the step kernel (fast tiers,
-// single GPU): the three stages' arguments exactly as do_stage builds them.
-// Returns HWG_EINVAL when the step kernel does not apply (the caller then
-// runs the three stage launches).
-int do_step(hwg_solver* s, double dt_hi, double dt_lo, long long step) {
-  if (!s->use_step || s->ddm || s->plo.on || s->phi.on || s->prog == nullptr ||
-      s->d.scheme != HWG_WENO5 || mode_of(s) == LIN)
-    return HWG_EINVAL;
-  StepArgs sa{};
-  auto r0 = [&](int r) -> double2* { return r >= 0 ? row0(s, r) : nullptr; };
-  for (int st = 0; st < 3; ++st) {
-    const Plan p = make_plan(s, HWG_SSPRK33, st, DD{dt_hi, dt_lo});
-    StageArgs& a = sa.st[st];
-    a = base_args(s);
-    a.step = step >= 0 ? step + 1 : -1;
-    a.bump = (step < 0 && st == 0) ? 1 : 0;
-    a.x = r0(p.x); a.o = r0(p.out); a.ua = r0(p.ua); a.ub = r0(p.ub); a.ug = r0(p.ug);
-    a.f = r0(p.f);
-    a.ca = p.ca.hi; a.cb = p.cb.hi; a.cc = p.cc.hi; a.cg = p.cg.hi; a.cd = p.cd.hi; a.ce = p.ce.hi;
-    if (p.epi == EPI_RK3C) a.tick = s->flag + 4;
-  }
-  sa.prog = s->prog;
-  sa.timeout_ns = 2000000000ll;  // 2 s: a stuck neighbour is a bug, not a slow peer
-  cudaError_t e = launch_step_fast(sa, s->d.scheme, mode_of(s), s->blocks, s->wpb, s->stream);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    s->err = std::string("step kernel launch: ") + cudaGetErrorString(e);
-    return HWG_ECUDA;
-  }
-  std::swap(s->cur, s->scr1);  // the RK3 rotation of the third stage (make_plan rot = 1)
-  return HWG_OK;
-}
-
 int ensure_staging(hwg_solver* s, size_t cnt) {
   if (s->stage_cap < cnt) {
     if (s->stage_dev) cudaFree(s->stage_dev);
@@ -742,12 +707,9 @@ int launch_steps_impl(hwg_solver* s, int stepper, double dt_hi, double dt_lo, lo
     int rc = ensure_regs(s, 5);
     if (rc) return rc;
   }
-  // one whole step: the step kernel where it applies, else ns stage launches
+  // one whole step: ns stage launches (a single cooperative launch of all
+  // three RK3 stages with neighbour dataflow was measured slower)
   auto one_step = [&](long long step) -> int {
-    if (stepper == HWG_SSPRK33) {
-      const int rc = do_step(s, dt_hi, dt_lo, step);
-      if (rc != HWG_EINVAL) return rc;
-    }
     for (int st = 0; st < ns; ++st) {
       const int rc = do_stage(s, stepper, st, dt_hi, dt_lo, step);
       if (rc) return rc;
@@ -863,7 +825,6 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   s->sigma = {d->sigma, ddm ? d->sigma_lo : 0.0};
   if (const char* e = std::getenv("HWG_NO_GRAPH")) s->use_graphs = e[0] == '0';
   if (const char* e = std::getenv("HWG_NO_PDL")) s->use_pdl = e[0] == '0';
-  if (const char* e = std::getenv("HWG_STEP_KERNEL")) s->use_step = e[0] == '1';
   auto fail = [&](int rc) {
     g_create_err = s->err;
     hwg_destroy(s);
@@ -965,11 +926,7 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
     while (s->wpb > 1 && warps / s->wpb < nsm) s->wpb /= 2;
     s->blocks = (int)((warps + s->wpb - 1) / s->wpb);
   }
-  if (!ddm) {  // step kernel progress words, one per (range, chunk) warp
-    const size_t nw = (size_t)s->nranges * s->nchunks;
-    CK(cudaMalloc(&s->prog, nw * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(s->prog, 0, nw * sizeof(unsigned long long), s->stream));
-  }
+
   CK(cudaStreamSynchronize(s->stream));
 #undef CK
 #define CK(call)                                                               \
@@ -1045,7 +1002,6 @@ void hwg_destroy(hwg_solver* s) {
   cudaFree(s->kdev);
   cudaFree(s->cot);
   cudaFree(s->flag);
-  if (s->prog) cudaFree(s->prog);
   cudaFree(s->stage_dev);
   cudaFree(s->obs_dev);
   cudaFree(s->obs_w);
@@ -1272,10 +1228,7 @@ int hwg_status(hwg_solver* s, int* blew, long long* step, int clear) {
       s->err = "peer halo wait timed out (a neighbour slab did not run the same stage)";
       return HWG_ERUNTIME;
     }
-    if (s->hflag[0] & 4ull) {
-      s->err = "step kernel: a neighbour warp's stage never completed (dataflow timeout)";
-      return HWG_ERUNTIME;
-    }
+
     return HWG_OK;
   });
 }

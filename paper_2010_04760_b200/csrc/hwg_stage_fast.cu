@@ -47,35 +47,6 @@ void init_attributes_fast() {
   (void)done;
 }
 
-template <int SCH, int MODE>
-cudaError_t launch_step_t(const StepArgs& a, int blocks, int wpb, cudaStream_t st) {
-  static bool attr = [] {
-    cudaFuncSetAttribute(step_kernel<SCH, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)step_smem_bytes());
-    return true;
-  }();
-  (void)attr;
-  // cooperative: every block resident at once (the warps wait on each other)
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(wpb * 32);
-  cfg.dynamicSmemBytes = step_smem_bytes(wpb);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, step_kernel<SCH, MODE>, a);
-}
-
-cudaError_t launch_step_fast(const StepArgs& a, int scheme, int mode, int blocks, int wpb,
-                             cudaStream_t stream) {
-  if (scheme == WENO5 && mode == MIXED) return launch_step_t<WENO5, MIXED>(a, blocks, wpb, stream);
-  if (scheme == WENO5 && mode == F64) return launch_step_t<WENO5, F64>(a, blocks, wpb, stream);
-  return cudaErrorNotSupported;
-}
-
 template <int MODE>
 static cudaError_t occupancy_mode(int* occ) {
   const size_t sm = stage_smem_bytes<EPI_RK3>();
