@@ -75,7 +75,8 @@ def main():
         s = tails.summary(rows, w)
         runs[tier] = rows
         late = {f"p_phi_{a:.0f}_{b:.0f}": tails.summary(rows, (a, b))["p_phi"]
-                for a, b in ((100, 200), (200, 300), (300, 400), (400, 500), (500, tau_end))}
+                for a, b in ((100, 200), (200, 300), (300, 400), (400, 500), (500, tau_end))
+                if b <= tau_end + 1e-9}
         out[tier] = dict(steps=st["steps_done"], blew_up=st["blew_up"], wall_s=wall, **late,
                          stage_updates_per_s=16384 * 128 * 3 * st["steps_done"] / st["wall_seconds"],
                          window=w, **s,

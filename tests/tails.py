@@ -45,6 +45,8 @@ def window_rel_drift(t, z, t0, t1):
     """window_rel_drift (diagnostics.hpp:125-128): (max - min) / |mean| of |z|."""
     m = (t >= t0) & (t <= t1)
     a = np.abs(z[m])
+    if a.size == 0:
+        return float("nan")
     return float((a.max() - a.min()) / abs(a.mean()))
 
 
@@ -73,7 +75,7 @@ def summary(rows, window):
     m = (tau >= t0) & (tau <= t1)
     return dict(p_phi=window_mean(tp, pp, t0, t1), p_dphi=window_mean(td, pd, t0, t1),
                 p_proj=window_mean(tq, pq, t0, t1),
-                charge=float(np.mean(np.abs(dphi[m]))),
+                charge=float(np.mean(np.abs(dphi[m]))) if m.any() else float("nan"),
                 charge_drift=window_rel_drift(tau, dphi, t0, t1))
 
 
