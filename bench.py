@@ -590,7 +590,8 @@ def main():
     ap.add_argument("--mode", default="mixed", choices=["mixed", "f64"])
     ap.add_argument("--nrho", type=int, default=65536)
     ap.add_argument("--ntheta", type=int, default=512)
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=32,
+                    help="independent e2e jobs timed (more jobs amortise the PCIe pipeline fill and drain)")
     ap.add_argument("--e2e-lanes", type=int, default=4,
                     help="independent e2e jobs in flight on one GPU (own handle + stream each)")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
