@@ -26,6 +26,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <exception>
 #include <stdexcept>
@@ -33,11 +34,11 @@
 #include <thread>
 #include <vector>
 
-#include "hweno/coeff_kernels.hpp"
 #include "hweno/evolve.hpp"
 #include "hweno/geometry.hpp"
 #include "hweno/timestep.hpp"
 #include "hweno_gpu.h"
+#include "hweno_gpu_setup.hpp"
 
 namespace hweno_gpu {
 
@@ -166,81 +167,6 @@ inline hweno::RunStats advance_steps(GpuEvolutionRhs& rhs, const hweno::StepperS
   rs.blew_up = st.blew_up != 0;
   rs.blowup_step = long(st.blowup_step);
   return rs;
-}
-
-// assemble_coefficients (proj/src/geometry.cpp:118-168) off the serial host
-// path: the same per-point double-double evaluation of the
-// reference's generated kernels (wave_op_coeffs, coeff_kernels.hpp:661-666),
-// theta rows split over host threads.  Bitwise identical to the serial
-// version: every point is computed independently and max_speed is an exact
-// max.  The first error in the serial (k, j) order is rethrown.
-inline hweno::CoefficientSet assemble_coefficients_parallel(const hweno::Grid& g,
-                                                            const hweno::PhysicalParams& p,
-                                                            int threads = 0) {
-  using hweno::WorkReal;
-  hweno::CoefficientSet c;
-  c.nrho = g.nrho;
-  c.ntheta = g.ntheta;
-  const size_t n = size_t(g.nrho) * g.ntheta;
-  for (auto* v : {&c.b, &c.lam, &c.w_re, &c.w_im, &c.bt_re, &c.bt_im, &c.c_re, &c.c_im, &c.ath,
-                  &c.p_mix, &c.r_rad, &c.br_re, &c.br_im, &c.bprime})
-    v->resize(n);
-  c.cotth.resize(g.ntheta);
-  for (int k = 0; k < g.ntheta; ++k) c.cotth[k] = g.costh[k] / g.sinth[k];
-  if (threads <= 0) threads = std::max(1u, std::thread::hardware_concurrency());
-  threads = std::min(threads, g.ntheta);
-  std::vector<WorkReal> vmax(threads, WorkReal(0));
-  std::vector<std::exception_ptr> err(g.ntheta);
-  auto rows = [&](int t) {
-    for (int k = t; k < g.ntheta; k += threads) {
-      try {
-        for (int j = 0; j < g.nrho; ++j) {
-          auto w = hweno::wave_op_coeffs<WorkReal>(g.rho[j], g.costh[k], p.M, p.a, p.S, p.spin,
-                                                   p.mmode);
-          const size_t i = c.index(j, k);
-          WorkReal P = w.a_tr, R = w.a_rr;
-          WorkReal disc2 = P * P + WorkReal(4) * R;
-          if (disc2.hi < 0.0)
-            throw std::runtime_error("hyperbolicity violated at rho=" +
-                                     std::to_string(g.rho[j].hi) + " theta=" +
-                                     std::to_string(g.theta[k].hi));
-          WorkReal disc = sqrt(disc2);
-          WorkReal b = -(P + disc) / WorkReal(2);
-          WorkReal lam = b + disc;
-          WorkReal bp = -(w.da_tr + (P * w.da_tr + WorkReal(2) * w.da_rr) / disc) / WorkReal(2);
-          c.b[i] = b;
-          c.lam[i] = lam;
-          c.bprime[i] = bp;
-          c.p_mix[i] = P;
-          c.r_rad[i] = R;
-          c.bt_re[i] = w.bt_re;
-          c.bt_im[i] = w.bt_im;
-          c.br_re[i] = w.br_re;
-          c.br_im[i] = w.br_im;
-          c.c_re[i] = w.c_re;
-          c.c_im[i] = w.c_im;
-          c.ath[i] = w.a_th;
-          c.w_re[i] = lam * bp + w.br_re - w.bt_re * b;
-          c.w_im[i] = w.br_im - w.bt_im * b;
-          WorkReal sp = max(abs(b), abs(lam));
-          if (vmax[t] < sp) vmax[t] = sp;
-        }
-      } catch (...) {
-        err[k] = std::current_exception();
-      }
-    }
-  };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < threads; ++t) pool.emplace_back(rows, t);
-  rows(0);
-  for (auto& th : pool) th.join();
-  for (int k = 0; k < g.ntheta; ++k)
-    if (err[k]) std::rethrow_exception(err[k]);
-  WorkReal m(0);
-  for (const auto& v : vmax)
-    if (m < v) m = v;
-  c.max_speed = m;
-  return c;
 }
 
 }  // namespace hweno_gpu

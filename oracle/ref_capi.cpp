@@ -26,6 +26,7 @@
 #include "hweno/io.hpp"
 #include "hweno/parallel.hpp"
 #include "hweno/timestep.hpp"
+#include "hweno_gpu_setup.hpp"  // the reference's assembly on host threads (sub-grids)
 
 using namespace hweno;
 
@@ -108,7 +109,10 @@ int ref_create_deeper(double M, double a, int spin, int mmode, double S, int nrh
     } else {
       h->g = make_grid(nrho, ntheta, h->p);
     }
-    h->cs = assemble_coefficients(h->g, h->p);
+    // the unmodified assemble_coefficients, serial or (workers > 1) on theta-row
+    // sub-grids from `workers` threads — bitwise the same planes
+    h->cs = workers > 1 ? hweno_gpu::assemble_coefficients_parallel(h->g, h->p, workers)
+                        : assemble_coefficients(h->g, h->p);
     h->spec.scheme = scheme == 0 ? Scheme::weno5
                      : scheme == 1 ? Scheme::weno3
                                    : Scheme::fd6ko;
@@ -345,7 +349,10 @@ int ref_run_config(const char* ini, int workers, double* out, long max_rows, lon
     auto h = std::make_unique<RefHandle>();
     h->p = cfg.phys;
     h->g = make_grid(cfg.nrho, cfg.ntheta, h->p);
-    h->cs = assemble_coefficients(h->g, h->p);
+    // the unmodified assemble_coefficients, serial or (workers > 1) on theta-row
+    // sub-grids from `workers` threads — bitwise the same planes
+    h->cs = workers > 1 ? hweno_gpu::assemble_coefficients_parallel(h->g, h->p, workers)
+                        : assemble_coefficients(h->g, h->p);
     h->spec = cfg.scheme;
     h->pool = std::make_unique<WorkerPool>(workers > 0 ? workers : cfg.workers);
     h->rhs = std::make_unique<EvolutionRhs>(h->g, h->cs, h->p, h->spec, *h->pool);

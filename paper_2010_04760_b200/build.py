@@ -27,7 +27,7 @@ NVCC_FLAGS = [
     # every multiply-add in the kernels is an explicit fma(): results do not
     # depend on inlining / contraction choices (slab bit-identity)
     "-fmad=false",
-    "-Xcompiler", "-fPIC,-ffp-contract=off",
+    "-Xcompiler", "-fPIC,-ffp-contract=off,-Wall,-Wmisleading-indentation",
 ]
 
 

@@ -809,9 +809,10 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ri
       double2 img = make_double2(__shfl_sync(kFull, ps.x, wsrc & 31),
                                  __shfl_sync(kFull, ps.y, wsrc & 31));
       // image column in the previous chunk (last chunk with one column)
-      if (!active && (wsrc < 0 || wsrc > 31))
+      if (!active && (wsrc < 0 || wsrc > 31)) {
         HWG_CHK(in_reg(a.x + (ptrdiff_t)j * rs + psi_off(k0 + wsrc), a.x, rs, n, 1));
         img = ld2(a.x + (ptrdiff_t)j * rs + psi_off(k0 + wsrc));
+      }
       if (!active) wv = wflip ? neg2(img) : img;
     }
     // the chunk's extended row E[i] = Psi(k0 - 2 + i), i < 36, in shared memory

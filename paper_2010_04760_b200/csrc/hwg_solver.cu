@@ -32,6 +32,10 @@ struct NvtxRange {
 
 namespace {
 thread_local std::string g_create_err;
+// CUDA-graph cache entries per handle (least recently used goes first)
+constexpr size_t kMaxGraphs = 8;
+// fused halo push: minimum rows per rho range (max(IL, R, halo) over the schemes)
+constexpr int kMinPeerRangeRows = 4;
 
 // Host double-double, an exact replica of the reference's DDReal operators
 // (proj/include/hweno/precision.hpp:16-115).  Like the reference, the host
@@ -551,6 +555,14 @@ int do_stage_part(hwg_solver* s, int stepper, int stage, double dt_hi, double dt
       }
     }
     int blocks = 0;
+    if (s->plo.on || s->phi.on) {
+      // fused halo push: only the first and last range wait for the
+      // neighbours' rows and only they push, so every range must span at
+      // least max(IL, R, h) = 4 rows — then no other range's window reaches
+      // a halo row and ranges 0 / last own the pushed output rows
+      a.nranges = std::min(s->nranges, std::max(1, s->n / kMinPeerRangeRows));
+      blocks = (int)(((long long)a.nranges * s->nchunks + s->wpb - 1) / s->wpb);
+    }
     if (row_lo != 0 || row_hi != s->n) {  // a part: ranges in proportion to its rows
       a.row_lo = row_lo;
       a.row_hi = row_hi;
@@ -563,8 +575,9 @@ int do_stage_part(hwg_solver* s, int stepper, int stage, double dt_hi, double dt
     if (!last && check) a.defer = 1;
     rc = launch(s, a, p.epi, blocks);
   }
-  if (last && p.rot == 1) std::swap(s->cur, s->scr1);
-  if (last && p.rot == 2) std::swap(s->cur, s->scr2);
+  // the host's register rotation follows the device only for launched stages
+  if (rc == HWG_OK && last && p.rot == 1) std::swap(s->cur, s->scr1);
+  if (rc == HWG_OK && last && p.rot == 2) std::swap(s->cur, s->scr2);
   return rc;
 }
 
@@ -729,10 +742,12 @@ int launch_steps_impl(hwg_solver* s, int stepper, double dt_hi, double dt_lo, lo
   for (; q + 2 <= nsteps; q += 2) {
     const int rot[5] = {s->cur, s->scr1, s->scr2, s->scr3, s->scr4};
     cudaGraphExec_t exec = nullptr;
-    for (auto& e : s->graphs)
-      if (e.stepper == stepper && e.dt_hi == dt_hi && e.dt_lo == dt_lo &&
-          std::equal(rot, rot + 5, e.rot)) {
-        exec = e.exec;
+    auto exec_it = s->graphs.end();
+    for (auto it = s->graphs.begin(); it != s->graphs.end(); ++it)
+      if (it->stepper == stepper && it->dt_hi == dt_hi && it->dt_lo == dt_lo &&
+          std::equal(rot, rot + 5, it->rot)) {
+        exec = it->exec;
+        exec_it = it;
         break;
       }
     if (!exec) {
@@ -741,16 +756,35 @@ int launch_steps_impl(hwg_solver* s, int stepper, double dt_hi, double dt_lo, lo
       int rc = HWG_OK;
       for (int k = 0; k < 2 && rc == HWG_OK; ++k) rc = one_step(-1);
       cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
-      if (rc) return rc;
-      if (ce != cudaSuccess) {
+      if (rc != HWG_OK || ce != cudaSuccess) {
+        // nothing of the capture ran: drop it and undo its host bookkeeping
+        if (g) cudaGraphDestroy(g);
+        s->cur = rot[0]; s->scr1 = rot[1]; s->scr2 = rot[2]; s->scr3 = rot[3]; s->scr4 = rot[4];
+        if (rc != HWG_OK) return rc;
         s->err = std::string("graph capture: ") + cudaGetErrorString(ce);
         return HWG_ECUDA;
       }
-      CK(cudaGraphInstantiate(&exec, g, 0));
+      cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
       cudaGraphDestroy(g);
+      if (ie != cudaSuccess) {
+        s->cur = rot[0]; s->scr1 = rot[1]; s->scr2 = rot[2]; s->scr3 = rot[3]; s->scr4 = rot[4];
+        s->err = std::string("graph instantiate: ") + cudaGetErrorString(ie);
+        return HWG_ECUDA;
+      }
       // the capture ran do_stage's host bookkeeping for 2 steps: the
-      // rotation is back where it started, as after a replay
+      // rotation is back where it started, as after a replay.  The cache is
+      // keyed by dt: an adaptive-dt caller would grow it without bound, so
+      // the least recently used entry goes once kMaxGraphs are held.
+      if (s->graphs.size() >= kMaxGraphs) {
+        cudaGraphExecDestroy(s->graphs.front().exec);
+        s->graphs.erase(s->graphs.begin());
+      }
       hwg_solver::GraphEntry e{stepper, dt_hi, dt_lo, {rot[0], rot[1], rot[2], rot[3], rot[4]}, exec};
+      s->graphs.push_back(e);
+    } else if (exec_it + 1 != s->graphs.end()) {
+      // most recently used at the back
+      hwg_solver::GraphEntry e = *exec_it;
+      s->graphs.erase(exec_it);
       s->graphs.push_back(e);
     }
     CK(cudaGraphLaunch(exec, s->stream));
@@ -1316,6 +1350,18 @@ int hwg_advance(hwg_solver* s, int stepper, double dt_hi, double dt_lo, long lon
       }
       return HWG_OK;
     };
+    {
+      // a blow-up flag left by an earlier call: the state is frozen, nothing
+      // steps (clear it with hwg_status(clear) or hwg_set_state first)
+      bool blown = false;
+      if ((rc = check_flag(blown)) == HWG_OK && blown) {
+        st.steps_done = 0;
+        st.wall_seconds = 0.0;
+        if (stats) *stats = st;
+        return HWG_OK;
+      }
+      if (rc) return rc;
+    }
     long long q = s0;
     for (;;) {
       const bool hook_now = hook && (q % every == 0 || q == s0 || q == s1);

@@ -2,7 +2,7 @@
 library (oracle/_ref/libhweno_ref.so, compiled in place from
 /root/reference/proj/src).  Run in the build container:
 
-    python tests/golden/make_golden.py [--big]
+    python tests/golden/make_golden.py [--big] [--c2]
 
 Small cases (npz, a few tens of KB each) pin one RHS evaluation and a short
 evolution in both reference modes (DD "full" and DD+fp64-weight "mixed") for
@@ -93,6 +93,32 @@ def _big(name, phys, nrho, ntheta, mode, steps, workers):
                         nrho=nrho, ntheta=ntheta)
 
 
+def _c2(workers, steps=1000, every=10):
+    """BASELINE configs[1] at its stated physics and size: extremal Kerr a=1,
+    s=-2, m=2, 4096x128, reference mixed, SSP-RK3.  Stores the final interior
+    .hi state, SHA-256 digests of the final DD state (hi and lo limbs, for
+    the bitwise dd-mixed check) and the reference HorizonSampler series at
+    k = Ntheta/2 every `every` steps (diagnostics.cpp:145-165; the Aretakis
+    charge is dphi[0], :162-165)."""
+    import hashlib
+    phys = Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22)
+    ref = RefSolver(phys, 4096, 128, scheme="weno5", mode="mixed", workers=workers)
+    u, ulo = ref.initial_data()
+    dt = ref.select_dt("ssprk33")
+    t0 = time.time()
+    (uf, ufl), st, obs = ref.advance(u, ulo, dt, 0, steps, hook_every=every, ktheta=64,
+                                     max_obs=steps // every + 2)
+    print("c2_mixed_1000", st, f"{time.time() - t0:.1f}s", flush=True)
+    hi = np.ascontiguousarray(uf[:, 2:-2, 4:-4])
+    lo = np.ascontiguousarray(ufl[:, 2:-2, 4:-4])
+    np.savez_compressed(os.path.join(HERE, "c2_mixed_1000.npz"), state=hi,
+                        sha_hi=np.frombuffer(hashlib.sha256(hi.tobytes()).digest(), np.uint8),
+                        sha_lo=np.frombuffer(hashlib.sha256(lo.tobytes()).digest(), np.uint8),
+                        horizon=obs, every=every, ktheta=64, dt=np.array(dt), drho=ref.drho,
+                        steps=steps, mode="mixed", nrho=4096, ntheta=128,
+                        wall=st["wall_seconds"], workers=workers)
+
+
 def main():
     only = [a for a in sys.argv[1:] if not a.startswith("--")]
     for c in SMALL:
@@ -106,6 +132,10 @@ def main():
              1024, 64, "full", 1000, workers)
         _big("c2desk_mixed_1000", Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0,
                                           width=0.22), 1024, 32, "mixed", 1000, workers)
+
+
+    if "--c2" in sys.argv:
+        _c2(os.cpu_count() or 8)
 
 
 if __name__ == "__main__":

@@ -163,6 +163,11 @@ def test_blowup_freezes_state(cuda_ok):
     one.launch_steps("ssprk33", dt, 0, 1)
     np.testing.assert_array_equal(interior(frozen), interior(one.get_state()))
     assert not np.all(np.isfinite(interior(frozen))) or np.max(np.abs(interior(frozen))) > 1e30
+    # a second call with the flag still set steps nothing (steps_done 0, the
+    # recorded blow-up step) and leaves the frozen state alone
+    st2 = gpu.advance("ssprk33", dt, 3, 6)
+    assert st2["blew_up"] and st2["steps_done"] == 0 and st2["blowup_step"] == 1
+    np.testing.assert_array_equal(interior(gpu.get_state()), interior(frozen))
 
 
 def test_stage_parts_equal_whole_stages(cuda_ok):
@@ -286,6 +291,67 @@ def test_c2desk_mixed_1000_steps_vs_reference_mixed(cuda_ok):
     got = interior(gpu.get_state())
     err = np.max(np.abs(got - fx["state"])) / np.max(np.abs(fx["state"]))
     assert err <= 1e-6, err
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c2_mixed_1000.npz")),
+                    reason="C2 fixture not generated")
+@pytest.mark.parametrize("tier", ["mixed", "dd-mixed"])
+def test_c2_1000_steps_and_aretakis_charge(cuda_ok, tier):
+    """BASELINE configs[1] at its stated physics AND size: extremal Kerr a=1,
+    s=-2, m=2, 4096x128, WENO5, 1000 SSP-RK3 steps against the reference's
+    own mixed mode (tests/golden/make_golden.py --c2).  GPU mixed (fp32
+    weights): state within 1e-6 normwise; the dd-mixed tier: the final DD
+    state bit for bit (SHA-256 of both limbs).  Aretakis charge extraction:
+    the reference HorizonSampler series (Phi, d_rho Phi .. at rho_+, row
+    Ntheta/2, every 10 steps; diagnostics.cpp:145-165) against the device
+    observers — the charge d_rho Phi within 1% (north_star; mixed) and to
+    1e-11 relative (dd-mixed)."""
+    import hashlib
+
+    import oracle as O
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
+    fx = load_golden("c2_mixed_1000")
+    phys = O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22)
+    ref = O.RefSolver(phys, 4096, 128, mode="mixed", workers=os.cpu_count() or 1)
+    hi, lo = ref.initial_data()
+    dt = (float(fx["dt"][0]), float(fx["dt"][1]))
+    assert dt == ref.select_dt("ssprk33")
+    k = int(fx["ktheta"])
+    j0, hw = ref.horizon_weights(k)
+    gpu = GpuEvolution.from_reference(ref, SchemeSpec("weno5", tier, ref.eps))
+    gpu.set_observers(k, j0, hw, 0, None)
+    gpu.set_state(hi, lo) if tier.startswith("dd") else gpu.set_state(hi)
+    got = []
+    every = int(fx["every"])
+    st = gpu.advance("ssprk33", dt, 0, int(fx["steps"]), every=every,
+                     hook=lambda s, tau, ob: got.append([tau[0], ob["phi"]] + list(ob["dphi"])))
+    assert st["steps_done"] == int(fx["steps"]) and not st["blew_up"]
+    ref_obs = fx["horizon"]
+    assert len(got) == len(ref_obs)
+    tau = np.array([g[0] for g in got])
+    np.testing.assert_array_equal(tau, ref_obs[:, 0])
+    obs = np.array([[v for z in g[1:] for v in (z.real, z.imag)] for g in got])
+    charge = obs[:, 2] + 1j * obs[:, 3]                    # d_rho Phi at the horizon
+    ref_charge = ref_obs[:, 3] + 1j * ref_obs[:, 4]
+    rel = np.max(np.abs(charge - ref_charge)) / np.max(np.abs(ref_charge))
+    phi_rel = (np.max(np.abs(obs[:, 0] + 1j * obs[:, 1] - (ref_obs[:, 1] + 1j * ref_obs[:, 2]))) /
+               np.max(np.abs(ref_obs[:, 1] + 1j * ref_obs[:, 2])))
+    print(tier, "charge rel", rel, "phi rel", phi_rel)
+    if tier == "mixed":
+        assert rel <= 0.01 and phi_rel <= 0.01
+        assert rel <= 1e-6  # in fact: the state gate's tolerance
+        got_state = interior(gpu.get_state())
+        err = np.max(np.abs(got_state - fx["state"])) / np.max(np.abs(fx["state"]))
+        print("state rel", err)
+        assert err <= 1e-6, err
+    else:
+        assert rel <= 1e-11 and phi_rel <= 1e-11
+        gh, gl = gpu.get_state_dd()
+        h = hashlib.sha256(np.ascontiguousarray(interior(gh)).tobytes()).digest()
+        l_ = hashlib.sha256(np.ascontiguousarray(interior(gl)).tobytes()).digest()
+        assert np.array_equal(interior(gh), fx["state"])
+        assert h == fx["sha_hi"].tobytes() and l_ == fx["sha_lo"].tobytes()
+    gpu.close()
 
 
 def test_c2_full_size_prefix_vs_reference(cuda_ok):
