@@ -114,81 +114,127 @@ def dist_env():
 
 
 # --------------------------------------------------------------------- reference arm
-def cpu_reference_rate(seconds: float, nrho=1024, ntheta=512, steps_cap=1000):
-    """The UNMODIFIED reference (oracle/_ref) on all host cores: its own
-    EvolutionRhs + advance_steps in mixed mode (DD state + fp64 weights), RK3,
-    hook off, on a bounded sample grid of the workload's physics.  Returns
-    (updates/s, cores, sample, kind)."""
+def host_info():
+    """CPU facts for the baseline record: usable cores and the load before the run."""
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = os.cpu_count() or 1
+    try:
+        load = os.getloadavg()[0]
+    except Exception:
+        load = None
+    return usable, load
+
+
+def reference_rates(nrho, ntheta, modes=("mixed",), warm=1, steps=3, workers=None):
+    """The UNMODIFIED reference (oracle/_ref) on the host cores, on the GPU
+    arm's own grid and physics (C5 shape: extremal Kerr a=1, s=-2, m=2,
+    WENO5, SSP-RK3, hook off, default FP environment): make_grid +
+    assemble_coefficients (on theta-row sub-grids from `workers` threads,
+    bitwise the serial result; untimed) + initial_data (untimed), then ONE
+    advance_steps call over warm + steps steps with a timestamp hook, as the
+    reference's bench-scaling harness does (proj/tools/main.cpp:168-221).
+    The first `warm` steps (they include the stepper's scratch allocation)
+    are excluded; the rate is P * 3 * steps / (sum of the timed steps).
+    Workers: all usable cores but one, so the pool's per-phase barriers do
+    not wait on a thread descheduled by the box's own processes."""
     import oracle as O
-    cores = os.cpu_count() or 1
-    if O.ref_available():
-        ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22),
-                          nrho, ntheta, mode="mixed", workers=cores)
+    usable, load = host_info()
+    workers = workers or max(1, usable - 1)
+    phys = O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22)
+    out = {}
+    for mode in modes:
+        t0 = time.perf_counter()
+        ref = O.RefSolver(phys, nrho, ntheta, mode=mode, workers=workers)
         u, lo = ref.initial_data()
-        dt = ref.select_dt()
-        # one step first (also warms the pool), then steps until `seconds`
-        ref.advance(u, lo, dt, 0, 1)
-        done, wall = 0, 0.0
-        (u, lo), st, _ = ref.advance(u, lo, dt, 0, 1)
-        done += 1
-        wall += st["wall_seconds"]
-        per = max(wall, 1e-3)
-        n = max(1, min(steps_cap, int(seconds / per)))
-        (u, lo), st, _ = ref.advance(u, lo, dt, 1, 1 + n)
-        done, wall = n, st["wall_seconds"]
-        rate = nrho * ntheta * 3 * done / wall
-        return rate, cores, f"{nrho}x{ntheta} grid, C5 physics (a=1, s=-2, m=2), reference mixed " \
-                            f"(DD state + fp64 weights), ssprk33, {done} steps, {wall:.1f} s", "reference"
-    # fall back to the C restatement (single thread)
+        setup = time.perf_counter() - t0
+        dt = ref.select_dt("ssprk33")
+        (u, lo), st, per = ref.advance_timed(u, lo, dt, 0, warm + steps)
+        if st["blew_up"]:
+            raise RuntimeError(f"reference {mode}: blew up")
+        timed = per[warm:]
+        wall = float(timed.sum())
+        out[mode] = {"value": nrho * ntheta * 3 * steps / wall, "unit": UNIT, "steps": steps,
+                     "warm_steps": warm, "wall_s": wall, "per_step_s": [float(x) for x in timed],
+                     "warm_step_s": [float(x) for x in per[:warm]], "setup_s": setup}
+        del ref, u, lo
+    return out, workers, usable, load
+
+
+def ref_sample(nrho, ntheta, mode, r, workers, usable):
+    return (f"{nrho}x{ntheta} grid (the GPU arm's per-GPU workload), C5 physics (a=1, s=-2, "
+            f"m=2), reference {mode} ({'DD state + fp64 weights' if mode == 'mixed' else 'DD'}), "
+            f"weno5, ssprk33, {r['steps']} steps timed after {r['warm_steps']} warm-up in one "
+            f"advance_steps call, {workers} pool workers of {usable} usable cores, "
+            f"{r['wall_s']:.1f} s")
+
+
+def cpu_reference_rate(nrho, ntheta, steps=3):
+    """The GPU arm's cpu_baseline: the reference arm's measurement (mixed,
+    same grid, same procedure), or the C restatement when oracle/_ref is absent."""
+    import oracle as O
+    if O.ref_available():
+        rr, workers, usable, load = reference_rates(nrho, ntheta, ("mixed",), 2, steps)
+        r = rr["mixed"]
+        return {"value": r["value"], "unit": UNIT, "cores": workers, "kind": "reference",
+                "sample": ref_sample(nrho, ntheta, "mixed", r, workers, usable),
+                "per_step_s": r["per_step_s"], "loadavg_before": load}
+    # fall back to the C restatement (single thread) on a bounded sample
     from paper_2010_04760_b200 import synthetic
-    prob = synthetic.problem(nrho, ntheta)
-    orc = O.OracleSolver(nrho, ntheta, prob["drho"], prob["dtheta"], prob["parity"],
+    n, nt = 1024, 512
+    prob = synthetic.problem(n, nt)
+    orc = O.OracleSolver(n, nt, prob["drho"], prob["dtheta"], prob["parity"],
                          prob["coef"], prob["cotth"], "weno5", "mixed")
     u = synthetic.initial_state(prob)
     t0 = time.time()
-    n = 0
-    while time.time() - t0 < seconds:
-        u, _ = orc.advance(u, synthetic.select_dt(prob), n, n + 1)
-        n += 1
+    k = 0
+    while time.time() - t0 < 10.0:
+        u, _ = orc.advance(u, synthetic.select_dt(prob), k, k + 1)
+        k += 1
     wall = time.time() - t0
-    return nrho * ntheta * 3 * n / wall, 1, f"{nrho}x{ntheta} synthetic, C restatement, {n} steps", "port"
+    return {"value": n * nt * 3 * k / wall, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{n}x{nt} synthetic, C restatement, {k} steps"}
 
 
 def run_reference(args):
     """--impl reference: the reference's own CPU implementation (oracle/_ref,
-    the unmodified library) on all host cores; one step = one SSP-RK3 step of
-    a bounded 1024x512 sample grid of the workload's physics."""
+    the unmodified library) on the host cores, on the GPU arm's config
+    (args.nrho x args.ntheta, C5 physics, WENO5, SSP-RK3), both reference
+    modes: mixed (the GPU mixed tier's parity reference and
+    the line's value) and full.  A reference step at this size takes seconds,
+    so the timed steps are capped (min(K, 3) after min(W, 2) warm-up) to keep
+    the run within a few minutes; the per-step times are reported."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     import oracle as O
-    cores = os.cpu_count() or 1
-    nrho, ntheta = args.ref_nrho, args.ntheta
+    nrho, ntheta = args.nrho, args.ntheta
+    K, W = min(args.steps, args.ref_steps), min(args.warmup, 2)
     if not O.ref_available():
-        r, cores, sample, kind = cpu_reference_rate(args.cpu_seconds)
-        v, wall, K = r, 0.0, args.steps
+        c = cpu_reference_rate(nrho, ntheta)
+        modes, v, kind, cores, sample = {}, c["value"], c["kind"], c["cores"], c["sample"]
+        wall = 0.0
     else:
-        kind = "reference"
-        ref = O.RefSolver(O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22),
-                          nrho, ntheta, mode="mixed", workers=cores)
-        u, lo = ref.initial_data()
-        dt = ref.select_dt()
-        (u, lo), _, _ = ref.advance(u, lo, dt, 0, args.warmup)
-        K = args.steps
-        (u, lo), st, _ = ref.advance(u, lo, dt, args.warmup, args.warmup + K)
-        wall = st["wall_seconds"]
-        v = nrho * ntheta * 3 * K / wall
-        sample = (f"{nrho}x{ntheta} grid, C5 physics (a=1, s=-2, m=2), reference mixed "
-                  f"(DD state + fp64 weights), ssprk33, {K} steps, {wall:.1f} s")
+        modes, workers, usable, load = reference_rates(nrho, ntheta, ("mixed", "full"), W, K)
+        r = modes["mixed"]
+        v, kind, cores, wall = r["value"], "reference", workers, r["wall_s"]
+        sample = ref_sample(nrho, ntheta, "mixed", r, workers, usable)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": K, "warmup": args.warmup, "ms_per_step": 1000 * wall / max(K, 1),
+            "steps": K, "steps_requested": args.steps, "warmup": W,
+            "ms_per_step": 1000 * wall / max(K, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "dd state, fp64 weights", "data": "synthetic",
-            "config": {"workload": f"C5 physics, bounded CPU sample {nrho}x{ntheta}",
-                       "scheme": "weno5", "stepper": "ssprk33", "mode": "reference mixed"},
+            "config": {"workload": f"C5 shape {nrho}x{ntheta} per GPU, C5 physics (a=1, s=-2, "
+                                   f"m=2), WENO5, SSP-RK3 (the B200 arm's workload)",
+                       "scheme": "weno5", "stepper": "ssprk33", "mode": "reference mixed",
+                       "same_config": True},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": sample},
+            "modes": modes,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if "full" in modes:
+        line["mixed_vs_full_speedup"] = modes["mixed"]["value"] / modes["full"]["value"]
     print(json.dumps(line), flush=True)
     return 0
 
@@ -515,8 +561,7 @@ def run_b200(args):
     shapes = config_rates(torch) if world == 1 and not args.no_configs else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r, cores, sample, kind = cpu_reference_rate(args.cpu_seconds)
-        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        cpu = cpu_reference_rate(args.nrho, args.ntheta)
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -596,11 +641,11 @@ def main():
                     help="independent e2e jobs in flight on one GPU (own handle + stream each)")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="N > 1 slab halos: fused push over NVLink peer memory, or NCCL P2P")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-steps", type=int, default=3,
+                    help="--impl reference: timed reference steps cap (seconds each at 65536x512)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dd", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
-    ap.add_argument("--ref-nrho", type=int, default=1024)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

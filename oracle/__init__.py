@@ -72,6 +72,8 @@ def ref_lib():
         lib.ref_select_dt.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp]
         lib.ref_advance.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, C.c_long, C.c_long,
                                     _dp, C.c_long, C.c_int, _dp, C.c_long, _lp, _dp]
+        lib.ref_advance_timed.argtypes = [C.c_void_p, C.c_int, C.c_double, _dp, C.c_long,
+                                          C.c_long, _dp, _dp, _lp]
         lib.ref_run_series.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_double,
                                        C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                        _dp, C.c_long, _lp, _dp]
@@ -234,6 +236,20 @@ class RefSolver:
         st = dict(steps_done=stats[0], blew_up=bool(stats[1]), blowup_step=stats[2],
                   n_obs=stats[3], wall_seconds=wall.value)
         return u, st, obs[: 9 * stats[3]].reshape(-1, 9)
+
+    def advance_timed(self, hi, lo, dt, s0, s1, stepper="ssprk33", cfl=0.5):
+        """One advance_steps call over [s0, s1) with a timestamp hook:
+        returns ((hi, lo), stats, per-step wall seconds (s1 - s0,))."""
+        dd = join_dd(hi, lo)
+        dtv = np.array([dt[0], dt[1]] if isinstance(dt, tuple) else [dt, 0.0])
+        stamps = np.zeros(s1 - s0 + 1)
+        stats = (C.c_long * 3)()
+        _chk(ref_lib().ref_advance_timed(self.h, STEPPERS[stepper], cfl, _ptr(dtv), s0, s1,
+                                         _ptr(dd), _ptr(stamps), stats))
+        del hi, lo
+        u = split_dd(dd, self.shape)
+        st = dict(steps_done=stats[0], blew_up=bool(stats[1]), blowup_step=stats[2])
+        return u, st, np.diff(stamps)
 
     def run_series(self, init: Physics, stepper="ssprk104", cfl=0.5, tau_end=500.0,
                    cadence=0.25, observer_rho=10.0, max_rows=200000):

@@ -12,6 +12,7 @@
 //   HorizonSampler / multipole_project     proj/src/diagnostics.cpp:128-283
 // No reference source is copied here; only its public headers are included.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -276,6 +277,35 @@ int ref_advance(void* hv, int stepper, double cfl, const double* dt_dd,
     stats[2] = rs.blowup_step;
     stats[3] = n_obs;
     if (wall) *wall = rs.wall_seconds;
+  });
+}
+
+// advance_steps [s0, s1) with the hook disabled except for a timestamp at
+// every step (SampleHook every = 1: fired before each step and at s1), so
+// stamps[i] - stamps[i-1] is the wall time of step s0 + i - 1 inside ONE
+// advance_steps call — the reference's own bench-scaling harness
+// (proj/tools/main.cpp:168-221) times one call the same way.  stamps: s1 - s0
+// + 1 seconds since the call began.  stats as ref_advance.
+int ref_advance_timed(void* hv, int stepper, double cfl, const double* dt_dd, long s0,
+                      long s1, double* u_dd, double* stamps, long* stats) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    StepperSpec st;
+    st.kind = stepper == 0 ? StepperSpec::ssprk33 : StepperSpec::ssprk104;
+    st.cfl = WorkReal(cfl);
+    StateVec u = from_dd(u_dd, h->rhs->layout().size());
+    WorkReal dt(dt_dd[0], dt_dd[1]);
+    SampleHook hook;
+    hook.every = 1;
+    const auto t0 = std::chrono::steady_clock::now();
+    hook.fn = [&](long s, const WorkReal&, const StateVec&) {
+      stamps[s - s0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    RunStats rs = advance_steps(*h->rhs, st, u, dt, s0, s1, hook, *h->pool);
+    to_dd(u, u_dd);
+    stats[0] = rs.steps_done;
+    stats[1] = rs.blew_up ? 1 : 0;
+    stats[2] = rs.blowup_step;
   });
 }
 

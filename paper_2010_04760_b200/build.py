@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 SO = os.path.join(PKG, "libhwgpu.so")
 CSRC = os.path.join(PKG, "csrc")
 SRCS = [os.path.join(CSRC, f) for f in ("hwg_solver.cu", "hwg_stage_fast.cu", "hwg_stage_dd.cu")]
-HDRS = [os.path.join(CSRC, f) for f in ("hwg_kernels.cuh", "hwg_dd.cuh", "hwg_launch.h",
+HDRS = [os.path.join(CSRC, f) for f in ("hwg_kernels.cuh", "hwg_dd.cuh", "hwg_dd_ops.h", "hwg_launch.h",
                                         "hwg_dispatch.cuh")] + [
     os.path.join(ROOT, "include", "hweno_gpu.h")]
 DEPS = SRCS + HDRS
