@@ -14,8 +14,8 @@ void launch_stage_fast(const StageArgs& a, int scheme, int mode, int epi, int bl
 // sets every kernel's smem attribute
 cudaError_t occupancy_fast(int* blocks_per_sm, int mode);
 void init_attributes_fast();
-// double-double tiers (stage_kernel_dd): ppb warp pairs per block
-void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks, int ppb,
+// double-double tiers (stage_kernel_dd)
+void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks, int wpb,
                      cudaStream_t stream);
 cudaError_t occupancy_dd(int* blocks_per_sm);
 void init_attributes_dd();

@@ -945,9 +945,8 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
     int nsm = 148, occ = 1;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->dev));
     CK(ddm ? occupancy_dd(&occ) : occupancy_fast(&occ, mode_of(s)));
-    // work units: one warp per (chunk, range) in the fast tiers, one warp
-    // PAIR in the double-double tiers
-    const int upb = ddm ? kPairsPerBlockDD : kWarpsPerBlock;
+    // work units: one warp per (theta chunk, rho range)
+    const int upb = kWarpsPerBlock;
     const long long target = (long long)nsm * std::max(occ, 1) * upb;
     long long nr = std::max<long long>(1, target / s->nchunks);
     // rows per range: as few as 2 on tiny grids to fill the wave (the window
@@ -959,7 +958,7 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
     s->nranges = (int)nr;
     // small grids: fewer warps per block so the warps spread over all SMs
     const long long units = nr * s->nchunks;
-    s->wpb = upb;  // units per block (warps, or warp pairs)
+    s->wpb = upb;  // warps per block
     while (s->wpb > 1 && units / s->wpb < nsm) s->wpb /= 2;
     s->blocks = (int)((units + s->wpb - 1) / s->wpb);
   }
@@ -1274,7 +1273,7 @@ int hwg_launch_info(const hwg_solver* s, int* blocks, int* threads, int* nranges
                     int* pitch) {
   return guarded(s, [&]() -> int {
     *blocks = s->blocks;
-    *threads = s->wpb * (s->ddm ? 64 : 32);
+    *threads = s->wpb * 32;
     *nranges = s->nranges;
     *nchunks = s->nchunks;
     *pitch = (int)s->rs;

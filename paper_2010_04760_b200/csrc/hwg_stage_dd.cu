@@ -10,16 +10,15 @@ struct DDLauncher {
     cudaFuncSetAttribute(stage_kernel_dd<SCH, MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)stage_smem_bytes_dd<EPI>());
   }
-  // ppb: warp PAIRS per block (one pair per theta chunk and rho range)
-  static void run(const StageArgsDD& a, int blocks, int ppb, cudaStream_t st) {
-    stage_kernel_dd<SCH, MODE, EPI><<<blocks, ppb * 64, stage_smem_bytes_dd<EPI>(ppb), st>>>(a);
+  static void run(const StageArgsDD& a, int blocks, int wpb, cudaStream_t st) {
+    stage_kernel_dd<SCH, MODE, EPI><<<blocks, wpb * 32, stage_smem_bytes_dd<EPI>(wpb), st>>>(a);
   }
 };
 }  // namespace
 
 void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks,
-                     int ppb, cudaStream_t stream) {
-  dispatch<DDLauncher>(a, scheme, mode, epi, blocks, ppb, stream);
+                     int wpb, cudaStream_t stream) {
+  dispatch<DDLauncher>(a, scheme, mode, epi, blocks, wpb, stream);
 }
 
 void init_attributes_dd() {
@@ -37,7 +36,7 @@ cudaError_t occupancy_dd(int* occ) {
                                        (int)stage_smem_bytes_dd<EPI_RK3>());
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, stage_kernel_dd<WENO5, F64, EPI_RK3>,
-                                                       kPairsPerBlockDD * 64,
+                                                       kWarpsPerBlock * 32,
                                                        stage_smem_bytes_dd<EPI_RK3>());
 }
 }  // namespace hwg
