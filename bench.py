@@ -305,13 +305,23 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # the overlapped NCCL path (interior rows, then the strips) is timed as
+    # the runner runs it, one event pair per step; otherwise one per stage
+    # launch (the fused peer push and single-GPU runs are whole-stage launches)
+    per_step = halo == "nccl-overlap"
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(ns * K)]
+           for _ in range(K if per_step else ns * K)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     i = 0
     for q in range(K):
+        if per_step:
+            evs[i][0].record(stream)
+            runner.step(stepper, dt, W + q)
+            evs[i][1].record(stream)
+            i += 1
+            continue
         for st in range(ns):
             runner.exchange(g.stage_input(stepper, st))
             evs[i][0].record(stream)
@@ -325,7 +335,7 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
         t = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    stage_ms = np.array([a.elapsed_time(b) for a, b in evs]).reshape(K, ns)
+    stage_ms = np.array([a.elapsed_time(b) for a, b in evs]).reshape(K, 1 if per_step else ns)
     blown, _ = g.status()
     if blown:
         raise RuntimeError(f"benchmark state blew up ({mode})")
@@ -338,6 +348,40 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
     achieved = bytes_per_step * K / (kern_ms / 1000.0) / 1e9
     return g, dict(value=value, total_ms=total_ms, stage_ms=stage_ms, achieved_gbs=achieved,
                    kern_ms=kern_ms, P=P, dt=dt, K=K, halo=halo, runner=runner)
+
+
+def sustained_mode(g, args, prob, dt, torch, clocks_cls, dev, warm_s=1.0, timed_s=2.5):
+    """The headline tier under sustained load: whole SSP-RK3 steps replayed
+    back to back (hwg_launch_steps, CUDA graphs) for >= warm_s untimed, then
+    >= timed_s timed with CUDA events and its own clock record (the 20-step
+    burst sits inside the power-cap transient)."""
+    stream = torch.cuda.current_stream()
+    P = prob["nrho"] * prob["ntheta"]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g.launch_steps("ssprk33", dt, 0, 20)
+    e0.record(stream)
+    g.launch_steps("ssprk33", dt, 20, 20)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    per = max(e0.elapsed_time(e1) / 20.0, 1e-3)
+    nw = max(20, int(warm_s * 1e3 / per))
+    nt = max(20, int(timed_s * 1e3 / per))
+    ck = clocks_cls(dev)
+    ck.start()
+    g.launch_steps("ssprk33", dt, 40, nw)
+    ck.mark()
+    e0.record(stream)
+    g.launch_steps("ssprk33", dt, 40 + nw, nt)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ck.mark()
+    ck.stop()
+    ms = e0.elapsed_time(e1)
+    blown, _ = g.status()
+    if blown:
+        raise RuntimeError("sustained run blew up")
+    return {"value": P * 3 * nt / (ms / 1e3), "ms_per_step": ms / nt, "steps": nt,
+            "warm_steps": nw, "timed_s": ms / 1e3, "clocks": ck.summary()}
 
 
 def _e2e_job(g, u, out, dt, q, runner=None):
@@ -424,13 +468,14 @@ def e2e_mode(g, args, prob, world, rank, torch, dist, dt, runner=None):
                                      get_state=1e3 * tot[2], wall_per_step=1e3 * wall / ke))
 
 
-def e2e_advance_mode(g, args, prob, dt, torch):
+def e2e_advance_mode(g, args, prob, dt, torch, K=None, every=1):
     """The drop-in's own usage of the boundary (the reference's driver calls
     advance_steps once per run, driver.cpp:93): one hwg_advance call over K
     steps with the HOST state in and out (pinned FieldLayout, hwg_set_state /
     hwg_get_state inside the timed region) and the observers read back to the
-    host at every step through the hook (every = 1; the reference samples at
-    round(0.25/dt)).  Reported beside the strict per-step round trip (e2e)."""
+    host through the hook every `every` steps (the reference's driver
+    samples every round(0.25/dt) steps, driver.cpp:40-49).  Reported beside
+    the strict per-step round trip (e2e)."""
     from paper_2010_04760_b200 import synthetic
     from paper_2010_04760_b200.hwgpu import HwgObservables, _lib, _p
     nrho, nth = prob["nrho"], prob["ntheta"]
@@ -441,26 +486,28 @@ def e2e_advance_mode(g, args, prob, dt, torch):
     u = torch.empty(g.shape, dtype=torch.float64, pin_memory=True).numpy()
     u[...] = synthetic.initial_state(prob)
     out = torch.empty(g.shape, dtype=torch.float64, pin_memory=True).numpy()
-    K = args.steps
+    K = args.steps if K is None else K
     seen = []
     hook = lambda step, tau, obs: seen.append(obs["dphi"][0])  # noqa: E731
     g.set_state(u)
-    g.advance("ssprk33", dt, 0, 2, every=1, hook=hook)      # warm
+    g.advance("ssprk33", dt, 0, 2, every=every, hook=hook)      # warm
     g._chk(_lib.hwg_get_state(g.h, _p(out)))
     seen.clear()
     t0 = time.perf_counter()
     g.set_state(u)
-    st = g.advance("ssprk33", dt, 0, K, every=1, hook=hook)
+    st = g.advance("ssprk33", dt, 0, K, every=every, hook=hook)
     g._chk(_lib.hwg_get_state(g.h, _p(out)))
     wall = time.perf_counter() - t0
-    if st["blew_up"] or st["steps_done"] != K or len(seen) != K + 1:
-        raise RuntimeError(f"e2e advance: {st}, {len(seen)} hook calls")
+    nhook = len(range(0, K, every)) + 1  # s % every == 0 for s < K, and s == K
+    if st["blew_up"] or st["steps_done"] != K or len(seen) != nhook:
+        raise RuntimeError(f"e2e advance: {st}, {len(seen)} hook calls (expected {nhook})")
     ob = ctypes.sizeof(HwgObservables)
     return {"value": nrho * nth * 3 * K / wall, "unit": UNIT,
             "h2d_bytes_per_step": u.nbytes / K,
-            "d2h_bytes_per_step": (out.nbytes + (K + 1) * ob) / K, "steps": K,
-            "path": "C ABI hwg_set_state + hwg_advance(K steps, observers to the host every "
-                    "step) + hwg_get_state, pinned host FieldLayout fp64"}
+            "d2h_bytes_per_step": (out.nbytes + len(seen) * ob) / K, "steps": K,
+            "hook_every": every, "hook_calls": len(seen),
+            "path": f"C ABI hwg_set_state + hwg_advance(K steps, observers to the host every "
+                    f"{every} step(s)) + hwg_get_state, pinned host FieldLayout fp64"}
 
 
 # the other BASELINE shapes (parity-test configurations; not the headline):
@@ -506,6 +553,44 @@ def config_rates(torch):
         out[label] = {"value": n * nt * 3 * K / (ms / 1e3), "ms_per_step": ms / K, "steps": K,
                       "l2": "resident (grid < L2)" if n * nt * 168 < 100e6 else "streams"}
     return out
+
+
+def fp64_peak():
+    """Measured FP64 lane-operations/s of this B200 (tools/fp_peaks.cu, the
+    DFMA/DADD throughput kernels; profiles/r02_fp_peaks.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_fp_peaks.json")) as f:
+            p = json.load(f)
+        return min(p["dfma"]["lane_ops_per_s"], p["dadd"]["lane_ops_per_s"]), "measured"
+    except Exception:
+        return 1.8e13, "fallback"
+
+
+def mode_record(m, r, peak):
+    """Per-tier line entry.  The fp64 / mixed tiers are HBM-bound: frac of
+    the copy peak.  The double-double tiers are FP64-pipe bound: their
+    roofline is the FP64 pipe — FP64 lane operations per point-stage (ncu
+    count of the SSP-RK3 middle-stage kernel, profiles/dd_fp64_ops.json)
+    x updates/s over the measured FP64 peak — and the HBM fraction is kept
+    for reference only."""
+    rec = {"value": r["value"], "ms_per_step": r["total_ms"] / r["K"], "steps": r["K"],
+           "stepper": "ssprk104" if m.endswith("ssprk104") else "ssprk33",
+           "stage_kernel_gbs": r["achieved_gbs"], "frac": r["achieved_gbs"] / peak,
+           "step_or_stage_ms_mean": [float(x) for x in r["stage_ms"].mean(axis=0)],
+           "halo": r["halo"]}
+    if m.startswith("dd"):
+        try:
+            with open(os.path.join(ROOT, "profiles", "dd_fp64_ops.json")) as f:
+                ops = json.load(f)[m]["fp64_lane_ops_per_point_stage"]
+        except Exception:
+            ops = None
+        fpk, src = fp64_peak()
+        rec["roofline"] = {"bound": "fp64", "unit": "FP64 lane-ops/s", "peak": fpk,
+                           "peak_source": src, "ops_per_point_stage": ops,
+                           "achieved": ops * r["value"] if ops else None,
+                           "frac": ops * r["value"] / fpk if ops else None}
+        rec["frac_hbm_for_reference"] = rec.pop("frac")
+    return rec
 
 
 def run_b200(args):
@@ -558,6 +643,16 @@ def run_b200(args):
             results[mode] = r
     e2e = e2e_mode(g, args, prob, world, rank, torch, dist, head["dt"], head["runner"])
     e2e_adv = e2e_advance_mode(g, args, prob, head["dt"], torch) if world == 1 else None
+    # the drop-in at the reference driver's observer cadence, round(0.25/dt)
+    # steps (driver.cpp:40-49), over two sampling periods
+    e2e_prod = None
+    if world == 1 and not args.no_sustained:
+        dt_hi = head["dt"][0] if isinstance(head["dt"], tuple) else float(head["dt"])
+        every = max(1, int(round(0.25 / dt_hi)))
+        e2e_prod = e2e_advance_mode(g, args, prob, head["dt"], torch, K=2 * every, every=every)
+    sustained = None
+    if world == 1 and not args.no_sustained:
+        sustained = sustained_mode(g, args, prob, head["dt"], torch, ClockSampler, dev)
     shapes = config_rates(torch) if world == 1 and not args.no_configs else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -605,14 +700,14 @@ def run_b200(args):
                 "path": "C ABI hwg_set_state + 1 RK3 step + hwg_get_state (pinned host "
                         "FieldLayout fp64); independent jobs, 'lanes' in flight"},
         "e2e_advance": e2e_adv,
+        "e2e_advance_production": e2e_prod,
+        "sustained": None if sustained is None else {
+            **sustained, "roofline_frac": sustained["value"] * 157.33 / 1e9 / peak,
+            "vs_burst": sustained["value"] / head["value"]},
         "other_configs": shapes,
         "gpu_launches": 3 * K,
         "launch": info,
-        "modes": {m: {"value": r["value"], "ms_per_step": r["total_ms"] / r["K"], "steps": r["K"],
-                      "stepper": "ssprk104" if m.endswith("ssprk104") else "ssprk33",
-                      "stage_kernel_gbs": r["achieved_gbs"], "frac": r["achieved_gbs"] / peak,
-                      "stage_ms_mean": [float(x) for x in r["stage_ms"].mean(axis=0)]}
-                  for m, r in results.items()},
+        "modes": {m: mode_record(m, r, peak) for m, r in results.items()},
         "mixed_vs_fp64_speedup": results["mixed"]["value"] / results["f64"]["value"],
     }
     if "dd-full" in results:
@@ -646,6 +741,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dd", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

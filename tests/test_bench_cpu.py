@@ -16,7 +16,7 @@ def test_reference_arm_json_contract():
     if not O.ref_available():
         pytest.skip("reference library not built")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                        "--steps", "2", "--warmup", "1", "--ntheta", "16", "--ref-nrho", "128"],
+                        "--steps", "2", "--warmup", "1", "--ntheta", "16", "--nrho", "128"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr
     line = json.loads(r.stdout.strip().splitlines()[-1])

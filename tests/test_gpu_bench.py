@@ -35,3 +35,9 @@ def test_bench_json_line_small_grid(cuda_ok):
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert {"f64", "mixed", "mixed-ssprk104"} <= set(d["modes"])
     assert "workload" in d["config"]
+    # sustained figure with its own clock record; the drop-in at the driver's
+    # observer cadence (round(0.25/dt) steps)
+    su = d["sustained"]
+    assert su["value"] > 0 and su["timed_s"] >= 2.0 and "sm_mhz" in su["clocks"]
+    ep = d["e2e_advance_production"]
+    assert ep["hook_every"] > 1 and ep["hook_calls"] == 3 and ep["value"] > 0
