@@ -106,6 +106,14 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+_T0 = time.time()
+
+
+def log(msg):
+    """Progress on stderr (the driver parses stdout's JSON line only)."""
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -356,6 +364,7 @@ def sustained_mode(g, args, prob, dt, torch, clocks_cls, dev, warm_s=1.0, timed_
     >= timed_s timed with CUDA events and its own clock record (the 20-step
     burst sits inside the power-cap transient)."""
     stream = torch.cuda.current_stream()
+    g.set_stream(stream.cuda_stream)  # e2e_mode may have moved the handle to its own stream
     P = prob["nrho"] * prob["ntheta"]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     g.launch_steps("ssprk33", dt, 0, 20)
@@ -364,8 +373,8 @@ def sustained_mode(g, args, prob, dt, torch, clocks_cls, dev, warm_s=1.0, timed_
     e1.record(stream)
     torch.cuda.synchronize()
     per = max(e0.elapsed_time(e1) / 20.0, 1e-3)
-    nw = max(20, int(warm_s * 1e3 / per))
-    nt = max(20, int(timed_s * 1e3 / per))
+    nw = min(100000, max(20, int(warm_s * 1e3 / per)))
+    nt = min(100000, max(20, int(timed_s * 1e3 / per)))
     ck = clocks_cls(dev)
     ck.start()
     g.launch_steps("ssprk33", dt, 40, nw)
@@ -456,6 +465,8 @@ def e2e_mode(g, args, prob, world, rank, torch, dist, dt, runner=None):
     wall = time.perf_counter() - t0
     for h in hs[1:]:
         h.close()
+    if lanes > 1:
+        g.set_stream(torch.cuda.current_stream().cuda_stream)
     if world > 1:
         t = torch.tensor([wall], device=f"cuda:{torch.cuda.current_device()}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -617,6 +628,7 @@ def run_b200(args):
     for mode in modes:
         if mode == modes[-1]:
             clocks.mark()
+        log(f"time_mode {mode}")
         g, r = time_mode(args, mode, prob, world, rank, dev, torch, dist)
         if mode == modes[-1]:
             clocks.mark()
@@ -629,6 +641,7 @@ def run_b200(args):
         if m != args.mode:
             handles.pop(m).close()
     # the reference's production stepper (all proj/configs/*.ini use ssprk104)
+    log("time_mode ssprk104")
     g4, r = time_mode(args, args.mode, prob, world, rank, dev, torch, dist,
                       steps=max(1, args.steps // 3), stepper="ssprk104")
     g4.close()
@@ -637,11 +650,14 @@ def run_b200(args):
     # reference library): the paper's mixed-vs-full experiment on B200
     if not args.no_dd:
         for mode in ("dd-mixed", "dd-full"):
+            log(f"time_mode {mode}")
             gd, r = time_mode(args, mode, prob, world, rank, dev, torch, dist,
                               steps=max(1, min(3, args.steps)), warmup=1)
             gd.close()
             results[mode] = r
+    log("e2e")
     e2e = e2e_mode(g, args, prob, world, rank, torch, dist, head["dt"], head["runner"])
+    log("e2e_advance")
     e2e_adv = e2e_advance_mode(g, args, prob, head["dt"], torch) if world == 1 else None
     # the drop-in at the reference driver's observer cadence, round(0.25/dt)
     # steps (driver.cpp:40-49), over two sampling periods
@@ -649,14 +665,19 @@ def run_b200(args):
     if world == 1 and not args.no_sustained:
         dt_hi = head["dt"][0] if isinstance(head["dt"], tuple) else float(head["dt"])
         every = max(1, int(round(0.25 / dt_hi)))
+        log(f"e2e_advance production cadence every {every}")
         e2e_prod = e2e_advance_mode(g, args, prob, head["dt"], torch, K=2 * every, every=every)
     sustained = None
     if world == 1 and not args.no_sustained:
+        log("sustained")
         sustained = sustained_mode(g, args, prob, head["dt"], torch, ClockSampler, dev)
+    log("other configs")
     shapes = config_rates(torch) if world == 1 and not args.no_configs else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        log("cpu baseline")
         cpu = cpu_reference_rate(args.nrho, args.ntheta)
+        log("done")
     if world > 1:
         dist.barrier()
     if rank != 0:
