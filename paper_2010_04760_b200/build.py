@@ -14,7 +14,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SO = os.path.join(PKG, "libhwgpu.so")
 CSRC = os.path.join(PKG, "csrc")
-SRCS = [os.path.join(CSRC, f) for f in ("hwg_solver.cu", "hwg_stage_fast.cu", "hwg_stage_dd.cu")]
+SRCS = [os.path.join(CSRC, f) for f in ("hwg_solver.cu", "hwg_stage_fast.cu", "hwg_stage_dd.cu",
+                                        "hwg_peer_emu.cu")]
 HDRS = [os.path.join(CSRC, f) for f in ("hwg_kernels.cuh", "hwg_dd.cuh", "hwg_dd_ops.h", "hwg_launch.h",
                                         "hwg_dispatch.cuh")] + [
     os.path.join(ROOT, "include", "hweno_gpu.h")]

@@ -463,10 +463,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// bounded spin until *ctr >= want; false on timeout
+// bounded spin until *ctr >= want; false on timeout.  A wait that had to
+// spin (the neighbour's rows were not there yet) is counted in *spun.
 static __device__ __noinline__ bool peer_wait(const unsigned long long* ctr, unsigned long long want,
-                                       long long timeout_ns) {
+                                       long long timeout_ns, unsigned long long* spun) {
   if (ld_acquire_sys(ctr) >= want) return true;
+  atomicAdd(spun, 1ull);
   const unsigned long long t0 = globaltimer();
   while (ld_acquire_sys(ctr) < want) {
     __nanosleep(200);
@@ -484,8 +486,8 @@ static __device__ __noinline__ void peer_wait_halos(unsigned long long* wait,
     const unsigned long long want = *(volatile const unsigned long long*)epoch *
                                     (unsigned long long)nchunks;
     bool ok = true;
-    if (lo) ok &= peer_wait(wait, want, timeout_ns);
-    if (hi) ok &= peer_wait(wait + 1, want, timeout_ns);
+    if (lo) ok &= peer_wait(wait, want, timeout_ns, flag + 8);
+    if (hi) ok &= peer_wait(wait + 1, want, timeout_ns, flag + 8);
     if (!ok) atomicOr(flag, 2ull);
     // the halo rows also arrive through the bulk-copy (async) proxy
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -522,15 +524,15 @@ static __device__ __noinline__ void peer_push_halos(const double2* o, double2* o
   }
 }
 
-// every warp of a launch takes a ticket; the last one publishes the pending
-// blow-up bit and advances the peer epoch
+// every warp of a launch (nw warps) takes a ticket; the last one publishes
+// the pending blow-up bit and advances the peer epoch
 static __device__ __noinline__ void launch_ticket(unsigned long long* tick,
                                                   unsigned long long* flag,
-                                                  unsigned long long* epoch) {
+                                                  unsigned long long* epoch,
+                                                  unsigned long long nw) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) {
     __threadfence();
-    const unsigned long long nw = (unsigned long long)gridDim.x * (blockDim.x >> 5);
     if (atomicAdd(tick, 1ull) == nw - 1) {
       __threadfence();
       if (atomicExch(flag + 3, 0ull) != 0ull) atomicOr(flag, 1ull);
@@ -542,7 +544,7 @@ static __device__ __noinline__ void launch_ticket(unsigned long long* tick,
 
 template <int SCH, int MODE, int EPI, class WaitIn>
 __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ring, uint32_t bar0,
-                                           double2* trow, WaitIn&& wait_in);
+                                           double2* trow, WaitIn&& wait_in, int bid);
 
 // shared memory of one warp for a whole-launch stage: its ring, its ring's
 // mbarriers, its theta row (stage_smem_bytes)
@@ -565,22 +567,26 @@ stage_kernel(const StageArgs a) {
   double2* trow;
   stage_layout<EPI>(ring, bar0, trow);
   // the previous stage's grid has completed; its writes are visible
-  if (!stage_body<SCH, MODE, EPI>(a, ring, bar0, trow, [] { pdl_wait(); })) return;  // frozen
+  if (!stage_body<SCH, MODE, EPI>(a, ring, bar0, trow, [] { pdl_wait(); }, blockIdx.x))
+    return;  // frozen
   // let the next stage's grid launch once this warp's rows are done (measured:
   // triggering at kernel start lets the next grid's waiting blocks take SM
   // slots early and costs 12 % at C5; triggering here gains 3-5 % on the
   // launch-bound small grids and is neutral at C5)
   pdl_trigger();
   if (a.tick != nullptr)
-    launch_ticket(a.tick, a.flag, (a.px.on_lo | a.px.on_hi) ? a.px.epoch : nullptr);
+    launch_ticket(a.tick, a.flag, (a.px.on_lo | a.px.on_hi) ? a.px.epoch : nullptr,
+                  (unsigned long long)gridDim.x * (blockDim.x >> 5));
 }
 
 // false: the state is frozen (an earlier step blew up) and nothing was done.
 // ring / bar0 / trow: this warp's shared memory; wait_in(): returns once the
-// stage's inputs written by other warps or grids are visible.
+// stage's inputs written by other warps or grids are visible; bid: this
+// block's index in the stage's launch (blockIdx.x, or the block's index
+// within its slab in the peer emulation kernel, hwg_peer_emu.cu).
 template <int SCH, int MODE, int EPI, class WaitIn>
 __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ring, uint32_t bar0,
-                                           double2* trow, WaitIn&& wait_in) {
+                                           double2* trow, WaitIn&& wait_in, int bid) {
   using Wn = Win<SCH>;
   using SlotT = Slot<EPI>;
   constexpr int SL = Wn::SL, PL = Wn::PL, R = Wn::R, SW = Wn::SW, PW = Wn::PW;
@@ -590,7 +596,7 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ri
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;                     // warps per block (1, 2 or 4)
-  const int gw = blockIdx.x * wpb + wib;
+  const int gw = bid * wpb + wib;
   const int chunk = gw % a.nchunks;
   const int range = gw / a.nchunks;
   const bool live = range < a.nranges;  // else the whole warp only takes its ticket
@@ -663,14 +669,14 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ri
         mbar_wait(bar0 + q * 8, 0);
       }
     // a frozen slab still releases its neighbours for this stage (no data)
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (a.px.on_lo | a.px.on_hi)) {
+    if (bid == 0 && threadIdx.x == 0 && (a.px.on_lo | a.px.on_hi)) {
       if (a.px.on_lo) peer_signal(a.px.sig_lo, (unsigned long long)a.nchunks);
       if (a.px.on_hi) peer_signal(a.px.sig_hi, (unsigned long long)a.nchunks);
       *a.px.epoch += 1ull;
     }
     return false;
   }
-  if (a.bump && blockIdx.x == 0 && threadIdx.x == 0) a.flag[2] += 1ull;  // step counter
+  if (a.bump && bid == 0 && threadIdx.x == 0) a.flag[2] += 1ull;  // step counter
   if (!live) return true;
   // boundary ranges: wait for the neighbours' halo rows of this stage
   if ((a.px.on_lo && range == 0) | (a.px.on_hi && range == a.nranges - 1))

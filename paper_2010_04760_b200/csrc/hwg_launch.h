@@ -19,4 +19,22 @@ void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int bl
                      cudaStream_t stream);
 cudaError_t occupancy_dd(int* blocks_per_sm);
 void init_attributes_dd();
+// multi-slab emulation of the fused halo push in one cooperative launch
+// (hwg_peer_emu.cu): slab k owns blocks [block0, block0 + blocks) and runs
+// the stage sequence args[gi % period] (a device array), epilogues epi[]
+constexpr int kMaxEmuSlabs = 8;
+constexpr int kMaxEmuPeriod = 20;  // two SSP-RK(10,4) steps
+struct EmuSlab {
+  const StageArgs* args;
+  int block0, blocks;
+  unsigned long long* bar;  // slab-local stage barrier (monotonic counter)
+};
+struct EmuArgs {
+  int nslabs, nstages, period;
+  int epi[kMaxEmuPeriod];
+  EmuSlab s[kMaxEmuSlabs];
+};
+// capacity: co-resident blocks of the emulation kernel on this device
+cudaError_t launch_peer_emu(const EmuArgs& m, int scheme, int mode, int blocks,
+                            cudaStream_t stream, int* capacity);
 }  // namespace hwg

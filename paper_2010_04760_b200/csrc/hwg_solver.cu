@@ -513,6 +513,60 @@ int do_stage(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo, 
   return do_stage_part(s, stepper, stage, dt_hi, dt_lo, step, 0, s->n, true, true);
 }
 
+// kernel arguments of one fast-tier stage (or one part of it: rows
+// [row_lo, row_hi)); *blocks_out: the launch's grid (0 = the handle's)
+StageArgs fast_stage_args(const hwg_solver* s, const Plan& p, int stage, long long step,
+                        int row_lo, int row_hi, bool first, bool last, int* blocks_out) {
+  const long long rec = step >= 0 ? step + 1 : -1;
+  const int bump = (step < 0 && stage == 0 && first) ? 1 : 0;
+  auto r0 = [&](int r) -> double2* { return r >= 0 ? row0(s, r) : nullptr; };
+  StageArgs a = base_args(s);
+  a.step = rec;
+  a.bump = bump;
+  a.x = r0(p.x); a.o = r0(p.out); a.ua = r0(p.ua); a.ub = r0(p.ub); a.ug = r0(p.ug);
+  a.f = r0(p.f);
+  a.ca = p.ca.hi; a.cb = p.cb.hi; a.cc = p.cc.hi; a.cg = p.cg.hi; a.cd = p.cd.hi; a.ce = p.ce.hi;
+  const bool check = p.epi == EPI_RK3C || p.epi == EPI_RK104_10;
+  if (s->plo.on || s->phi.on) {
+    PeerArgs& x = a.px;
+    x.h = halo_rows(s->d.scheme);
+    x.wait = s->flag + 6;
+    x.epoch = s->flag + 5;
+    x.timeout_ns = s->peer_timeout_ns;
+    if (s->plo.on) {
+      x.on_lo = 1;
+      x.o_lo = s->plo.reg[p.out] + (size_t)(kHalo + s->plo.n) * s->rs;
+      x.sig_lo = s->plo.flag + 7;
+    }
+    if (s->phi.on) {
+      x.on_hi = 1;
+      x.o_hi = s->phi.reg[p.out] + (size_t)(kHalo - x.h) * s->rs;
+      x.sig_hi = s->phi.flag + 6;
+    }
+  }
+  int blocks = 0;
+  if (s->plo.on || s->phi.on) {
+    // fused halo push: only the first and last range wait for the
+    // neighbours' rows and only they push, so every range must span at
+    // least max(IL, R, h) = 4 rows — then no other range's window reaches
+    // a halo row and ranges 0 / last own the pushed output rows
+    a.nranges = std::min(s->nranges, std::max(1, s->n / kMinPeerRangeRows));
+    blocks = (int)(((long long)a.nranges * s->nchunks + s->wpb - 1) / s->wpb);
+  }
+  if (row_lo != 0 || row_hi != s->n) {  // a part: ranges in proportion to its rows
+    a.row_lo = row_lo;
+    a.row_hi = row_hi;
+    const int span = row_hi - row_lo;
+    a.nranges = (int)std::max<long long>(
+        1, std::min<long long>((long long)s->nranges * span / s->n, span / 2));
+    blocks = (int)(((long long)a.nranges * s->nchunks + s->wpb - 1) / s->wpb);
+  }
+  if (last && (check || s->plo.on || s->phi.on)) a.tick = s->flag + 4;
+  if (!last && check) a.defer = 1;
+  *blocks_out = blocks;
+  return a;
+}
+
 int do_stage_part(hwg_solver* s, int stepper, int stage, double dt_hi, double dt_lo,
                   long long step, int row_lo, int row_hi, bool first, bool last) {
   const Plan p = make_plan(s, stepper, stage, DD{dt_hi, dt_lo});
@@ -530,49 +584,8 @@ int do_stage_part(hwg_solver* s, int stepper, int stage, double dt_hi, double dt
     a.k.cg = to_dev(p.cg); a.k.cd = to_dev(p.cd); a.k.ce = to_dev(p.ce);
     rc = launch(s, a, p.epi);
   } else {
-    StageArgs a = base_args(s);
-    a.step = rec;
-    a.bump = bump;
-    a.x = r0(p.x); a.o = r0(p.out); a.ua = r0(p.ua); a.ub = r0(p.ub); a.ug = r0(p.ug);
-    a.f = r0(p.f);
-    a.ca = p.ca.hi; a.cb = p.cb.hi; a.cc = p.cc.hi; a.cg = p.cg.hi; a.cd = p.cd.hi; a.ce = p.ce.hi;
-    const bool check = p.epi == EPI_RK3C || p.epi == EPI_RK104_10;
-    if (s->plo.on || s->phi.on) {
-      PeerArgs& x = a.px;
-      x.h = halo_rows(s->d.scheme);
-      x.wait = s->flag + 6;
-      x.epoch = s->flag + 5;
-      x.timeout_ns = s->peer_timeout_ns;
-      if (s->plo.on) {
-        x.on_lo = 1;
-        x.o_lo = s->plo.reg[p.out] + (size_t)(kHalo + s->plo.n) * s->rs;
-        x.sig_lo = s->plo.flag + 7;
-      }
-      if (s->phi.on) {
-        x.on_hi = 1;
-        x.o_hi = s->phi.reg[p.out] + (size_t)(kHalo - x.h) * s->rs;
-        x.sig_hi = s->phi.flag + 6;
-      }
-    }
     int blocks = 0;
-    if (s->plo.on || s->phi.on) {
-      // fused halo push: only the first and last range wait for the
-      // neighbours' rows and only they push, so every range must span at
-      // least max(IL, R, h) = 4 rows — then no other range's window reaches
-      // a halo row and ranges 0 / last own the pushed output rows
-      a.nranges = std::min(s->nranges, std::max(1, s->n / kMinPeerRangeRows));
-      blocks = (int)(((long long)a.nranges * s->nchunks + s->wpb - 1) / s->wpb);
-    }
-    if (row_lo != 0 || row_hi != s->n) {  // a part: ranges in proportion to its rows
-      a.row_lo = row_lo;
-      a.row_hi = row_hi;
-      const int span = row_hi - row_lo;
-      a.nranges = (int)std::max<long long>(
-          1, std::min<long long>((long long)s->nranges * span / s->n, span / 2));
-      blocks = (int)(((long long)a.nranges * s->nchunks + s->wpb - 1) / s->wpb);
-    }
-    if (last && (check || s->plo.on || s->phi.on)) a.tick = s->flag + 4;
-    if (!last && check) a.defer = 1;
+    const StageArgs a = fast_stage_args(s, p, stage, step, row_lo, row_hi, first, last, &blocks);
     rc = launch(s, a, p.epi, blocks);
   }
   // the host's register rotation follows the device only for launched stages
@@ -885,8 +898,10 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
   CK(cudaMalloc(&s->cot, 2 * s->ntp * sizeof(double)));
   // [0] blown (bit 1: peer timeout) [1] blowup step [2] step counter [3] pending
   // blow-up [4] launch ticket [5] peer epoch [6] / [7] arrivals from lower / upper
-  CK(cudaMalloc(&s->flag, 8 * sizeof(unsigned long long)));
-  CK(cudaMemsetAsync(s->flag, 0, 8 * sizeof(unsigned long long), s->stream));
+  // [0] blown [1] blow-up step [2] step counter [3] pending [4] ticket [5] peer
+  // epoch [6,7] peer arrivals from lower / upper [8] peer waits that spun
+  CK(cudaMalloc(&s->flag, 16 * sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(s->flag, 0, 16 * sizeof(unsigned long long), s->stream));
   CK(cudaMallocHost(&s->hflag, 2 * sizeof(unsigned long long)));
   CK(cudaMallocHost(&s->obs_host, 16 * sizeof(double)));
   CK(cudaMalloc(&s->obs_dev, 16 * sizeof(double)));
@@ -1123,7 +1138,7 @@ int hwg_set_peers(hwg_solver* s, const hwg_peer_desc* lower, const hwg_peer_desc
     // counters, epoch and ticket restart at 0; graphs baked the old peer args
     for (auto& e : s->graphs) cudaGraphExecDestroy(e.exec);
     s->graphs.clear();
-    CK(cudaMemsetAsync(s->flag + 4, 0, 4 * sizeof(unsigned long long), s->stream));
+    CK(cudaMemsetAsync(s->flag + 4, 0, 5 * sizeof(unsigned long long), s->stream));
     CK(cudaStreamSynchronize(s->stream));
     return HWG_OK;
   });
@@ -1413,6 +1428,99 @@ int hwg_launch_stage_rows(hwg_solver* s, int stepper, int stage, double dt_hi, d
     }
     return do_stage_part(s, stepper, stage, dt_hi, dt_lo, step, row_lo, row_hi,
                          (part & HWG_PART_FIRST) != 0, (part & HWG_PART_LAST) != 0);
+  });
+}
+
+int hwg_peer_stats(hwg_solver* s, long long* spun) {
+  return guarded(s, [&]() -> int {
+    unsigned long long v = 0;
+    CK(cudaMemcpy(&v, s->flag + 8, sizeof(v), cudaMemcpyDeviceToHost));
+    *spun = (long long)v;
+    return HWG_OK;
+  });
+}
+
+int hwg_peer_emulate_steps(hwg_solver* const* slabs, int nslabs, int stepper, double dt_hi,
+                           double dt_lo, long long step0, long long nsteps) {
+  if (slabs == nullptr || nslabs < 1 || nslabs > kMaxEmuSlabs || slabs[0] == nullptr)
+    return HWG_EINVAL;
+  hwg_solver* s0 = slabs[0];
+  return guarded(s0, [&]() -> int {
+    NvtxRange nvtx_("hwg_peer_emulate_steps");
+    cudaSetDevice(s0->dev);
+    const int ns = stepper == HWG_SSPRK33 ? 3 : 10;
+    for (int k = 0; k < nslabs; ++k) {
+      hwg_solver* s = slabs[k];
+      if (s == nullptr || s->ddm || s->dev != s0->dev || s->d.scheme != s0->d.scheme ||
+          mode_of(s) != mode_of(s0) || nsteps < 0) {
+        s0->err = "hwg_peer_emulate_steps: fast-tier slabs of one scheme/precision on one device";
+        return HWG_EINVAL;
+      }
+      if (stepper == HWG_SSPRK104) {
+        int rc = ensure_regs(s, 5);
+        if (rc) return rc;
+      }
+    }
+    EmuArgs m{};
+    m.nslabs = nslabs;
+    m.period = 2 * ns;  // the register rotation repeats every two steps
+    m.nstages = (int)(nsteps * ns);
+    std::vector<StageArgs> host((size_t)nslabs * m.period);
+    int total = 0;
+    const DD dt{dt_hi, dt_lo};
+    for (int k = 0; k < nslabs; ++k) {
+      hwg_solver* s = slabs[k];
+      const int rot[5] = {s->cur, s->scr1, s->scr2, s->scr3, s->scr4};
+      for (int q = 0; q < m.period; ++q) {
+        const int stage = q % ns;
+        const Plan p = make_plan(s, stepper, stage, dt);
+        int blocks = 0;
+        host[(size_t)k * m.period + q] =
+            fast_stage_args(s, p, stage, -1, 0, s->n, true, true, &blocks);
+        m.epi[q] = p.epi;
+        if (p.rot == 1) std::swap(s->cur, s->scr1);
+        if (p.rot == 2) std::swap(s->cur, s->scr2);
+      }
+      s->cur = rot[0]; s->scr1 = rot[1]; s->scr2 = rot[2]; s->scr3 = rot[3]; s->scr4 = rot[4];
+      const long long warps = (long long)host[(size_t)k * m.period].nranges * s->nchunks;
+      m.s[k].block0 = total;
+      m.s[k].blocks = (int)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+      total += m.s[k].blocks;
+    }
+    StageArgs* dargs = nullptr;
+    unsigned long long* dbar = nullptr;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMalloc(&dargs, host.size() * sizeof(StageArgs));
+    if (e == cudaSuccess) e = cudaMalloc(&dbar, nslabs * sizeof(unsigned long long));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(dargs, host.data(), host.size() * sizeof(StageArgs), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(dbar, 0, nslabs * sizeof(unsigned long long));
+    for (int k = 0; k < nslabs && e == cudaSuccess; ++k) {
+      m.s[k].args = dargs + (size_t)k * m.period;
+      m.s[k].bar = dbar + k;
+      set_counter_kernel<<<1, 1, 0, s0->stream>>>(slabs[k]->flag + 2, step0);
+      e = cudaGetLastError();
+    }
+    int capacity = 0;
+    if (e == cudaSuccess)
+      e = launch_peer_emu(m, s0->d.scheme, mode_of(s0), total, s0->stream, &capacity);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s0->stream);
+    if (dargs) cudaFree(dargs);
+    if (dbar) cudaFree(dbar);
+    if (e != cudaSuccess) {
+      s0->err = std::string("hwg_peer_emulate_steps: ") + cudaGetErrorString(e) + " (" +
+                std::to_string(total) + " blocks, " + std::to_string(capacity) +
+                " co-resident)";
+      return HWG_ECUDA;
+    }
+    // the host's register rotation after nsteps steps
+    for (int k = 0; k < nslabs; ++k)
+      for (long long q = 0; q < nsteps * ns; ++q) {
+        const Plan p = make_plan(slabs[k], stepper, (int)(q % ns), dt);
+        if (p.rot == 1) std::swap(slabs[k]->cur, slabs[k]->scr1);
+        if (p.rot == 2) std::swap(slabs[k]->cur, slabs[k]->scr2);
+      }
+    return HWG_OK;
   });
 }
 

@@ -98,6 +98,9 @@ _lib.hwg_peer_export.argtypes = [_vp, C.POINTER(HwgPeerDesc)]
 _lib.hwg_set_peers.argtypes = [_vp, C.POINTER(HwgPeerDesc), C.POINTER(HwgPeerDesc), C.c_int,
                                C.c_double]
 _lib.hwg_peer_prime.argtypes = [_vp]
+_lib.hwg_peer_stats.argtypes = [_vp, C.POINTER(C.c_longlong)]
+_lib.hwg_peer_emulate_steps.argtypes = [C.POINTER(_vp), C.c_int, C.c_int, C.c_double, C.c_double,
+                                        C.c_longlong, C.c_longlong]
 
 EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg_set_stream", "hwg_set_state_dd",
             "hwg_get_state_dd", "hwg_set_state", "hwg_get_state", "hwg_rhs", "hwg_rhs_dd",
@@ -105,7 +108,7 @@ EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg
             "hwg_launch_steps", "hwg_stage_input", "hwg_register_ptr",
             "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize",
             "hwg_peer_export", "hwg_set_peers", "hwg_peer_prime", "hwg_abort_advance",
-            "hwg_launch_stage_rows"]
+            "hwg_launch_stage_rows", "hwg_peer_stats", "hwg_peer_emulate_steps"]
 
 
 class HwgError(RuntimeError):
@@ -353,6 +356,12 @@ class GpuEvolution:
     def peer_prime(self):
         self._chk(_lib.hwg_peer_prime(self.h))
 
+    def peer_stats(self) -> int:
+        """Boundary-warp waits that had to spin since hwg_set_peers."""
+        v = C.c_longlong()
+        self._chk(_lib.hwg_peer_stats(self.h, C.byref(v)))
+        return v.value
+
 
 def stage_bytes(stepper: str, mode: str = "mixed") -> float:
     """Algorithmic HBM bytes per grid point per stage: fp64
@@ -360,3 +369,15 @@ def stage_bytes(stepper: str, mode: str = "mixed") -> float:
     double-double tiers move twice that."""
     b = (136 + 168 + 168) / 3.0 if stepper == "ssprk33" else 1520 / 10.0
     return 2 * b if mode.startswith("dd") else b
+
+
+def peer_emulate_steps(handles, stepper: str, dt, step_begin: int, nsteps: int):
+    """hwg_peer_emulate_steps: peer-connected slab handles on one device run
+    `nsteps` steps in ONE cooperative launch (validation of the fused halo
+    push under genuine concurrency; include/hweno_gpu.h)."""
+    dt_hi, dt_lo = (dt if isinstance(dt, tuple) else (float(dt), 0.0))
+    arr = (_vp * len(handles))(*[h.h for h in handles])
+    rc = _lib.hwg_peer_emulate_steps(arr, len(handles), STEPPERS[stepper], dt_hi, dt_lo,
+                                     step_begin, nsteps)
+    if rc != 0:
+        handles[0]._chk(rc)

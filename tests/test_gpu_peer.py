@@ -17,7 +17,7 @@ from conftest import load_golden
 pytestmark = pytest.mark.gpu
 
 
-def _whole_and_slabs(g, mode, nslabs, stream=None):
+def _whole_and_slabs(g, mode, nslabs, stream=None, parts=None):
     from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
     from paper_2010_04760_b200.slabs import partition
     n, nt = int(g["nrho"]), int(g["ntheta"])
@@ -26,7 +26,7 @@ def _whole_and_slabs(g, mode, nslabs, stream=None):
                          g["coef"], g["cotth"], spec)
     whole.set_state(g["u0"])
     slabs = []
-    for off, cnt in partition(n, nslabs):
+    for off, cnt in (parts or partition(n, nslabs)):
         h = GpuEvolution(cnt, nt, float(g["drho"]), float(g["dtheta"]), int(g["parity"]),
                          g["coef"], g["cotth"], spec, rho_offset=off, nrho_global=n)
         u = np.zeros((4, nt + 4, cnt + 8))
@@ -55,6 +55,50 @@ def test_peer_slabs_bit_identical(cuda_ok, case, nslabs):
             assert h.status() == (False, -1)
             got = h.get_state()
             np.testing.assert_array_equal(got[:, 2:-2, 4:-4], ref[:, 2:-2, 4 + off:4 + off + cnt])
+        for _, _, h in slabs:
+            h.close()
+        whole.close()
+
+
+@pytest.mark.parametrize("case,parts", [
+    ("kerr09_w5", [(0, 24), (24, 48), (72, 24)]),              # uneven: neighbours drift
+    ("kerr09_w5", [(0, 16), (16, 16), (32, 32), (64, 32)]),
+    ("extremal_w5_theta34", [(0, 40), (40, 80), (120, 40)]),   # 2 theta chunks
+    ("extremal_fd6ko", [(0, 20), (20, 44)]),                   # halo 4
+    ("kerr09_w5_rk104", [(0, 64), (64, 16), (80, 16)])])       # SSP-RK(10,4)
+def test_peer_slabs_concurrent_emulation(cuda_ok, case, parts):
+    """The fused halo push under GENUINE concurrency: all slabs
+    run in one cooperative launch (hwg_peer_emulate_steps), ordered only by
+    the in-kernel pushes and arrival counters, as on separate GPUs.  Repeated
+    runs must reproduce the single-handle result bit for bit, no wait may
+    time out, and boundary warps must actually have spun on counters bumped
+    by running neighbours (hwg_peer_stats)."""
+    from paper_2010_04760_b200.slabs import LocalPeerSlabs
+    g = load_golden(case)
+    stepper = str(g["stepper"])
+    dt = (float(g["dt"][0]), float(g["dt"][1]))
+    K = 6
+    reps = 100 if case == "kerr09_w5" else 25
+    for mode in ("f64", "mixed"):
+        whole, slabs = _whole_and_slabs(g, mode, len(parts), parts=parts)
+        whole.launch_steps(stepper, dt, 0, K)
+        ref = whole.get_state()
+        ps = LocalPeerSlabs([h for _, _, h in slabs], timeout_s=5.0)
+        spun = 0
+        for rep in range(reps):
+            for off, cnt, h in slabs:
+                u = np.zeros((4, int(g["ntheta"]) + 4, cnt + 8))
+                u[:, 2:-2, 4:-4] = g["u0"][:, 2:-2, 4 + off:4 + off + cnt]
+                h.set_state(u)
+            ps.prime()
+            ps.steps_concurrent(stepper, dt, 0, K)
+            for off, cnt, h in slabs:
+                assert h.status() == (False, -1), (rep, off)
+                np.testing.assert_array_equal(h.get_state()[:, 2:-2, 4:-4],
+                                              ref[:, 2:-2, 4 + off:4 + off + cnt])
+        spun = sum(h.peer_stats() for _, _, h in slabs)
+        print(case, mode, parts, "spinning waits:", spun)
+        assert spun > 0
         for _, _, h in slabs:
             h.close()
         whole.close()
