@@ -31,6 +31,7 @@ struct EmuSlab {
 };
 struct EmuArgs {
   int nslabs, nstages, period;
+  long long skew_ns;  // odd slabs start every stage this much later (forces waits)
   int epi[kMaxEmuPeriod];
   EmuSlab s[kMaxEmuSlabs];
 };

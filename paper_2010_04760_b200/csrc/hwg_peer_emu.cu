@@ -13,8 +13,9 @@
 // — the in-kernel pushes into the neighbours' halo rows, their release
 // counters and the boundary warps' bounded acquire spins (stage_body,
 // hwg_kernels.cuh).  Slabs of different sizes drift apart, so boundary warps
-// genuinely wait on counters bumped by concurrently running blocks; the
-// spins are counted (flag[8], hwg_peer_stats).
+// genuinely wait on counters bumped by concurrently running blocks (with
+// skew_ns > 0 the odd slabs also start every stage late, so the even slabs'
+// boundary warps must wait); the spins are counted (flag[8], hwg_peer_stats).
 #include "hwg_launch.h"
 
 namespace hwg {
@@ -39,6 +40,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 1) peer_emu_kernel(const 
   const int bid = (int)blockIdx.x - S.block0;
   const unsigned long long nw = (unsigned long long)S.blocks * (blockDim.x >> 5);
   for (int gi = 0; gi < m.nstages; ++gi) {
+    if (m.skew_ns > 0 && (sl & 1)) {  // a late neighbour (test knob)
+      if (threadIdx.x == 0) {
+        const unsigned long long t0 = globaltimer();
+        while ((long long)(globaltimer() - t0) < m.skew_ns) __nanosleep(256);
+      }
+      __syncthreads();
+    }
     const StageArgs& a = S.args[gi % m.period];  // device copy (global memory)
     switch (m.epi[gi % m.period]) {
       case EPI_AXPY: emu_run<SCH, MODE, EPI_AXPY>(a, bid, nw); break;

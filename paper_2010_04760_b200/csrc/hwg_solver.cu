@@ -1441,7 +1441,7 @@ int hwg_peer_stats(hwg_solver* s, long long* spun) {
 }
 
 int hwg_peer_emulate_steps(hwg_solver* const* slabs, int nslabs, int stepper, double dt_hi,
-                           double dt_lo, long long step0, long long nsteps) {
+                           double dt_lo, long long step0, long long nsteps, long long skew_ns) {
   if (slabs == nullptr || nslabs < 1 || nslabs > kMaxEmuSlabs || slabs[0] == nullptr)
     return HWG_EINVAL;
   hwg_solver* s0 = slabs[0];
@@ -1465,6 +1465,7 @@ int hwg_peer_emulate_steps(hwg_solver* const* slabs, int nslabs, int stepper, do
     m.nslabs = nslabs;
     m.period = 2 * ns;  // the register rotation repeats every two steps
     m.nstages = (int)(nsteps * ns);
+    m.skew_ns = skew_ns;
     std::vector<StageArgs> host((size_t)nslabs * m.period);
     int total = 0;
     const DD dt{dt_hi, dt_lo};

@@ -100,7 +100,7 @@ _lib.hwg_set_peers.argtypes = [_vp, C.POINTER(HwgPeerDesc), C.POINTER(HwgPeerDes
 _lib.hwg_peer_prime.argtypes = [_vp]
 _lib.hwg_peer_stats.argtypes = [_vp, C.POINTER(C.c_longlong)]
 _lib.hwg_peer_emulate_steps.argtypes = [C.POINTER(_vp), C.c_int, C.c_int, C.c_double, C.c_double,
-                                        C.c_longlong, C.c_longlong]
+                                        C.c_longlong, C.c_longlong, C.c_longlong]
 
 EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg_set_stream", "hwg_set_state_dd",
             "hwg_get_state_dd", "hwg_set_state", "hwg_get_state", "hwg_rhs", "hwg_rhs_dd",
@@ -371,13 +371,14 @@ def stage_bytes(stepper: str, mode: str = "mixed") -> float:
     return 2 * b if mode.startswith("dd") else b
 
 
-def peer_emulate_steps(handles, stepper: str, dt, step_begin: int, nsteps: int):
+def peer_emulate_steps(handles, stepper: str, dt, step_begin: int, nsteps: int,
+                       skew_ns: int = 0):
     """hwg_peer_emulate_steps: peer-connected slab handles on one device run
     `nsteps` steps in ONE cooperative launch (validation of the fused halo
     push under genuine concurrency; include/hweno_gpu.h)."""
     dt_hi, dt_lo = (dt if isinstance(dt, tuple) else (float(dt), 0.0))
     arr = (_vp * len(handles))(*[h.h for h in handles])
     rc = _lib.hwg_peer_emulate_steps(arr, len(handles), STEPPERS[stepper], dt_hi, dt_lo,
-                                     step_begin, nsteps)
+                                     step_begin, nsteps, skew_ns)
     if rc != 0:
         handles[0]._chk(rc)

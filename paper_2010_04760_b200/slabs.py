@@ -184,12 +184,12 @@ class LocalPeerSlabs:
         for q in range(nsteps):
             self.step(stepper, dt, step_begin + q)
 
-    def steps_concurrent(self, stepper: str, dt, step_begin: int, nsteps: int):
+    def steps_concurrent(self, stepper: str, dt, step_begin: int, nsteps: int, skew_ns: int = 0):
         """All slabs' stages in ONE cooperative launch (hwg_peer_emulate_steps):
         the slabs run concurrently and are ordered only by the fused push's
         counters, as on separate GPUs — boundary warps really wait."""
         from .hwgpu import peer_emulate_steps
-        peer_emulate_steps(self.bs, stepper, dt, step_begin, nsteps)
+        peer_emulate_steps(self.bs, stepper, dt, step_begin, nsteps, skew_ns)
 
 
 class LocalSlabs:

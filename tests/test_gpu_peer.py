@@ -72,7 +72,8 @@ def test_peer_slabs_concurrent_emulation(cuda_ok, case, parts):
     the in-kernel pushes and arrival counters, as on separate GPUs.  Repeated
     runs must reproduce the single-handle result bit for bit, no wait may
     time out, and boundary warps must actually have spun on counters bumped
-    by running neighbours (hwg_peer_stats)."""
+    by running neighbours (hwg_peer_stats; every other run the odd slabs start
+    each stage 20 us late, so their neighbours' boundary warps must wait)."""
     from paper_2010_04760_b200.slabs import LocalPeerSlabs
     g = load_golden(case)
     stepper = str(g["stepper"])
@@ -91,7 +92,8 @@ def test_peer_slabs_concurrent_emulation(cuda_ok, case, parts):
                 u[:, 2:-2, 4:-4] = g["u0"][:, 2:-2, 4 + off:4 + off + cnt]
                 h.set_state(u)
             ps.prime()
-            ps.steps_concurrent(stepper, dt, 0, K)
+            # every other run with the odd slabs late at every stage
+            ps.steps_concurrent(stepper, dt, 0, K, skew_ns=20000 if rep % 2 else 0)
             for off, cnt, h in slabs:
                 assert h.status() == (False, -1), (rep, off)
                 np.testing.assert_array_equal(h.get_state()[:, 2:-2, 4:-4],
