@@ -63,16 +63,31 @@ class DistSlab:
         self.right = rank + 1 if rank < world - 1 else None
         self.h = HALO_ROWS[scheme]
         self.group = group
+        self._copy_back = []
         # interior / strips need >= 2 rows each (hwg_launch_stage_rows)
         self.overlap = (overlap and world > 1 and hasattr(backend, "launch_stage_rows")
                         and backend.nrho >= 2 * self.h + 2)
 
-    def post(self, reg: int):
-        """Post the halo exchange of register `reg`; returns the requests."""
+    def _staged(self, t) -> bool:
+        """Device rows over a host-only backend (gloo): exchange through host
+        copies (NCCL moves device rows directly)."""
         import torch.distributed as dist
+        return t.is_cuda and dist.get_backend(self.group) != "nccl"
+
+    def post(self, reg: int):
+        """Post the halo exchange of register `reg`; returns the requests
+        (pass them to wait())."""
+        import torch.distributed as dist
+        self._copy_back = []
         if self.world == 1:
             return []
         sl, rl, sr, rr = halo_views(self.b, reg, self.h)
+        if self._staged(sl):
+            self.b.synchronize()  # the stage that wrote the rows is done
+            host = lambda t: t.cpu()  # noqa: E731
+            rl_h, rr_h = rl.cpu(), rr.cpu()
+            self._copy_back = [(rl, rl_h), (rr, rr_h)]
+            sl, sr, rl, rr = host(sl), host(sr), rl_h, rr_h
         ops = []
         if self.left is not None:
             ops.append(dist.P2POp(dist.isend, sl, self.left, self.group))
@@ -82,9 +97,18 @@ class DistSlab:
             ops.append(dist.P2POp(dist.irecv, rr, self.right, self.group))
         return dist.batch_isend_irecv(ops)
 
-    def exchange(self, reg: int):
-        for req in self.post(reg):
+    def wait(self, reqs):
+        for req in reqs:
             req.wait()
+        if self._copy_back:
+            import torch
+            for dev, hst in self._copy_back:
+                dev.copy_(hst)
+            torch.cuda.synchronize()  # rows in place before the handle's next launch
+            self._copy_back = []
+
+    def exchange(self, reg: int):
+        self.wait(self.post(reg))
 
     def step(self, stepper: str, dt, step: int):
         ns = 3 if stepper == "ssprk33" else 10
@@ -92,16 +116,14 @@ class DistSlab:
         for st in range(ns):
             reqs = self.post(self.b.stage_input(stepper, st))
             if not self.overlap:
-                for req in reqs:
-                    req.wait()
+                self.wait(reqs)
                 self.b.launch_stage(stepper, st, dt, step)
                 continue
             # interior rows while the halo rows are in flight (NCCL: the
             # kernel is queued behind nothing but the previous stage; wait()
             # then orders the strips after the exchange on the device)
             self.b.launch_stage_rows(stepper, st, dt, step, h, n - h, True, False)
-            for req in reqs:
-                req.wait()
+            self.wait(reqs)
             self.b.launch_stage_rows(stepper, st, dt, step, 0, h, False, False)
             self.b.launch_stage_rows(stepper, st, dt, step, n - h, n, False, True)
 
