@@ -701,7 +701,9 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": head["total_ms"] / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 state, fp32 WENO weights" if args.mode == "mixed" else "f64",
-        "data": "synthetic (BASELINE shape; synthetic coefficient planes, Gaussian pulse)",
+        "data": "synthetic (BASELINE shape; synthetic coefficient planes with the reference's "
+                "structure, Gaussian pulse; on the reference's real C5 planes the same kernels "
+                "run at 1.016x this rate: tools/real_planes_bench.py, profiles/r02_real_planes.json)",
         "config": {"workload": f"C5 shape {args.nrho}x{args.ntheta} per GPU (radial slabs of "
                                f"{args.nrho * world}x{args.ntheta}), WENO5 {args.mode}, SSP-RK3",
                    "grid_points_per_gpu": head["P"], "stages_per_step": 3,

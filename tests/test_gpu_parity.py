@@ -387,6 +387,38 @@ def test_c2_full_size_prefix_vs_reference(cuda_ok):
             dd.close()
 
 
+def test_c4_full_size_prefix_vs_reference(cuda_ok):
+    """BASELINE configs[3]: FD6 + KO8 (sigma = 0.01) on the C2 extremal-Kerr
+    grid (a=1, s=-2, m=2, 4096x128), the reference run live on the box's
+    cores: GPU f64 vs reference full <= 1e-12 and the dd-full tier bit for
+    bit after 10 SSP-RK3 steps (FD6/KO8 have no weights, so the reference's
+    two modes coincide); the accuracy side of configs[3] is criterion 8's
+    scheme ranking (test_gpu_physics.py)."""
+    import oracle as O
+    from paper_2010_04760_b200.hwgpu import GpuEvolution, SchemeSpec
+    phys = O.Physics(a=1.0, spin=-2, mmode=2, ell=2, center=1.0, width=0.22)
+    ref = O.RefSolver(phys, 4096, 128, scheme="fd6ko", mode="full", sigma=0.01,
+                      workers=os.cpu_count() or 1)
+    hi, lo = ref.initial_data()
+    dt = ref.select_dt("ssprk33")
+    (rh, rl), st, _ = ref.advance(hi, lo, dt, 0, 10)
+    assert st["steps_done"] == 10 and not st["blew_up"]
+    gpu = GpuEvolution.from_reference(ref, SchemeSpec("fd6ko", "f64", ref.eps, 0.01))
+    gpu.set_state(hi)
+    gpu.advance("ssprk33", dt, 0, 10)
+    err = rel_linf(gpu.get_state(), rh)
+    print("C4 fd6ko f64 vs reference full:", err)
+    assert err <= 1e-12
+    gpu.close()
+    dd = GpuEvolution.from_reference(ref, SchemeSpec("fd6ko", "dd-full", ref.eps, 0.01))
+    dd.set_state(hi, lo)
+    dd.advance("ssprk33", dt, 0, 10)
+    gh, gl = dd.get_state_dd()
+    assert np.array_equal(interior(gh).view(np.uint64), interior(rh).view(np.uint64))
+    assert np.array_equal(interior(gl).view(np.uint64), interior(rl).view(np.uint64))
+    dd.close()
+
+
 @pytest.mark.parametrize("case,nslabs", [("kerr09_w5", 2), ("kerr09_w5", 3), ("extremal_w5_theta34", 2),
                                          ("extremal_fd6ko", 2), ("kerr09_w5_rk104", 2)])
 @pytest.mark.parametrize("overlap", [False, True])

@@ -194,3 +194,21 @@ def test_blowup_semantics():
     assert not orc.admissible(u)
     _, st = orc.advance(u, float(g["dt"][0]), 0, 5)
     assert st == dict(steps_done=1, blew_up=True, blowup_step=1)
+
+
+def test_threaded_assembly_bitwise_equals_serial():
+    """include/hweno_gpu_setup.hpp: the reference's own
+    assemble_coefficients on theta-row sub-grids from a thread pool gives the
+    serial planes bit for bit (hi and lo limbs, cot theta, max_speed -> dt)."""
+    import oracle as O
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    for phys in (O.Physics(a=1.0, spin=-2, mmode=2), O.Physics(a=0.9, spin=-2, mmode=0),
+                 O.Physics(a=0.0, spin=0, mmode=0)):
+        serial = O.RefSolver(phys, 96, 13, workers=1)
+        threaded = O.RefSolver(phys, 96, 13, workers=4)
+        for a, b in ((serial.coef, threaded.coef), (serial.coef_lo, threaded.coef_lo),
+                     (serial.cotth, threaded.cotth), (serial.cotth_lo, threaded.cotth_lo)):
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+        assert serial.max_speed == threaded.max_speed
+        assert serial.select_dt("ssprk33") == threaded.select_dt("ssprk33")
