@@ -18,6 +18,9 @@ void init_attributes_fast();
 void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks, int wpb,
                      cudaStream_t stream);
 cudaError_t occupancy_dd(int* blocks_per_sm);
+// self-test of the DD tier's branch-free division vs IEEE division
+cudaError_t div_selftest(long long n, unsigned long long seed, long long* mismatches,
+                         long long* guard_fails);
 void init_attributes_dd();
 // multi-slab emulation of the fused halo push in one cooperative launch
 // (hwg_peer_emu.cu): slab k owns blocks [block0, block0 + blocks) and runs

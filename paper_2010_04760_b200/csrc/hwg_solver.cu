@@ -1525,6 +1525,13 @@ int hwg_peer_emulate_steps(hwg_solver* const* slabs, int nslabs, int stepper, do
   });
 }
 
+int hwg_selftest_division(long long n, unsigned long long seed, long long* mismatches,
+                          long long* guard_fails) {
+  if (mismatches == nullptr || guard_fails == nullptr || n < 0) return HWG_EINVAL;
+  const cudaError_t e = div_selftest(n, seed, mismatches, guard_fails);
+  return e == cudaSuccess ? HWG_OK : HWG_ECUDA;
+}
+
 int hwg_abort_advance(hwg_solver* s) {
   if (s == nullptr) return HWG_EINVAL;
   s->abort_req = true;

@@ -98,6 +98,8 @@ _lib.hwg_peer_export.argtypes = [_vp, C.POINTER(HwgPeerDesc)]
 _lib.hwg_set_peers.argtypes = [_vp, C.POINTER(HwgPeerDesc), C.POINTER(HwgPeerDesc), C.c_int,
                                C.c_double]
 _lib.hwg_peer_prime.argtypes = [_vp]
+_lib.hwg_selftest_division.argtypes = [C.c_longlong, C.c_ulonglong, C.POINTER(C.c_longlong),
+                                       C.POINTER(C.c_longlong)]
 _lib.hwg_peer_stats.argtypes = [_vp, C.POINTER(C.c_longlong)]
 _lib.hwg_peer_emulate_steps.argtypes = [C.POINTER(_vp), C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_longlong, C.c_longlong, C.c_longlong]
@@ -108,7 +110,8 @@ EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg
             "hwg_launch_steps", "hwg_stage_input", "hwg_register_ptr",
             "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize",
             "hwg_peer_export", "hwg_set_peers", "hwg_peer_prime", "hwg_abort_advance",
-            "hwg_launch_stage_rows", "hwg_peer_stats", "hwg_peer_emulate_steps"]
+            "hwg_launch_stage_rows", "hwg_peer_stats", "hwg_peer_emulate_steps",
+            "hwg_selftest_division"]
 
 
 class HwgError(RuntimeError):
@@ -382,3 +385,13 @@ def peer_emulate_steps(handles, stepper: str, dt, step_begin: int, nsteps: int,
                                      step_begin, nsteps, skew_ns)
     if rc != 0:
         handles[0]._chk(rc)
+
+
+def selftest_division(n: int, seed: int = 1):
+    """hwg_selftest_division: (mismatches, guard_fails) of the DD tiers'
+    branch-free division against IEEE division on n random operand pairs."""
+    m, f = C.c_longlong(), C.c_longlong()
+    rc = _lib.hwg_selftest_division(n, seed, C.byref(m), C.byref(f))
+    if rc != 0:
+        raise HwgError(f"hwg_selftest_division failed ({rc})")
+    return m.value, f.value
