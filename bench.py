@@ -609,8 +609,20 @@ def run_b200(args):
     import torch.distributed as dist
     world, rank, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        # test plumbing only (tests/test_gpu_bench.py): all ranks on GPU 0 with
+        # a host-only backend, so the multi-rank control flow (slab
+        # partition, halo exchange, max-over-ranks timing, rank-0 line) runs
+        # on a 1-GPU box; never the fused push there (kernels would wait on
+        # each other on one GPU) — --halo nccl with DistSlab's staged exchange
+        backend = os.environ.get("HWG_BENCH_BACKEND", "nccl")
+        local_dev = 0 if os.environ.get("HWG_BENCH_ONE_GPU") else local
+        torch.cuda.set_device(local_dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_dev}"))
+        else:
+            if args.halo == "peer":
+                raise SystemExit("HWG_BENCH_BACKEND=gloo needs --halo nccl")
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()

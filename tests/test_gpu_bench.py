@@ -41,3 +41,33 @@ def test_bench_json_line_small_grid(cuda_ok):
     assert su["value"] > 0 and su["timed_s"] >= 2.0 and "sm_mhz" in su["clocks"]
     ep = d["e2e_advance_production"]
     assert ep["hook_every"] > 1 and ep["hook_calls"] == 3 and ep["value"] > 0
+
+
+def test_bench_two_ranks_control_flow_one_gpu(cuda_ok):
+    """bench.py's N > 1 path (radial slabs, per-stage halo exchange, the
+    overlapped NCCL-style sequence, max-over-ranks timing, rank-0 JSON line,
+    e2e through the slabs, the DD tiers' serial exchange) run as 2 ranks under
+    torchrun on this 1-GPU box: both ranks on GPU 0 with the gloo backend and
+    the host-staged exchange (HWG_BENCH_BACKEND / HWG_BENCH_ONE_GPU test
+    plumbing; no kernel waits on another).  The numbers are meaningless (two
+    processes share one GPU); the control flow is what the driver's
+    multi-GPU runs execute."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, HWG_BENCH_BACKEND="gloo", HWG_BENCH_ONE_GPU="1")
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+         "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+         "--gpus", "2", "--nrho", "1024", "--ntheta", "64", "--steps", "3", "--warmup", "3",
+         "--halo", "nccl", "--no-cpu", "--no-configs", "--no-sustained", "--e2e-steps", "2"],
+        capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["config"]["halo"] == "nccl-overlap"
+    assert d["modes"]["dd-mixed"]["halo"] == "nccl"
+    assert d["e2e"]["value"] > 0
