@@ -705,6 +705,13 @@ def run_b200(args):
             traffic = tj.get(key)
         except Exception:
             traffic = None
+    pipes = None
+    pf = os.path.join(ROOT, "profiles", "stage_kernel_pipes.json")
+    if os.path.exists(pf):
+        try:
+            pipes = json.load(open(pf)).get(f"{args.mode}_{args.nrho}x{args.ntheta}")
+        except Exception:
+            pipes = None
     ach = head["achieved_gbs"]
     info = g.launch_info()
     K = args.steps
@@ -726,6 +733,10 @@ def run_b200(args):
                      "frac": ach / peak, "traffic": traffic, "peak_source": src,
                      "kernel": "hwg::stage_kernel<WENO5>",
                      "bytes_per_point_stage": 157.33,
+                     # FP64 / FP32 / XU pipe and issue utilisation of the
+                     # three SSP-RK3 stage kernels (ncu --set full; the
+                     # weight computation's pipes, north_star)
+                     "pipes": pipes,
                      # secondary denominator: the B200 HBM3e datasheet figure
                      "frac_of_spec_8000_gbs": ach / 8000.0},
         "clocks": clocks.summary(),

@@ -49,6 +49,8 @@ def main():
         args = [a for a in args if a != tag]
     tfile = os.path.join(ROOT, "profiles", "stage_kernel_traffic.json")
     traffic = json.load(open(tfile)) if os.path.exists(tfile) else {}
+    pfile = os.path.join(ROOT, "profiles", "stage_kernel_pipes.json")
+    pipes = json.load(open(pfile)) if os.path.exists(pfile) else {}
     for rep in args:
         name = os.path.basename(rep).replace(".ncu-rep", "")
         hdr, units, rows = raw(rep)
@@ -56,6 +58,7 @@ def main():
                  "| launch | " + " | ".join(k for _, k in KEYS) + " | stalls (top 4) |",
                  "|---" * (len(KEYS) + 2) + "|"]
         tot_bytes = []
+        pipe_rows = []
         for r in rows:
             kn = r[hdr.index("Kernel Name")]
             vals = []
@@ -74,6 +77,14 @@ def main():
             tot = sum(v for v, _ in st) or 1
             top = ", ".join(f"{h} {100 * v / tot:.0f}%" for v, h in sorted(st, reverse=True)[:4])
             lines.append(f"| {kn} | " + " | ".join(vals) + f" | {top} |")
+            pr = {}
+            for m, k in (("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pct"),
+                         ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma_fp32_pct"),
+                         ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "xu_pct"),
+                         ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_pct")):
+                if m in hdr:
+                    pr[k] = round(float(r[hdr.index(m)]), 1)
+            pipe_rows.append(pr)
         mean = sum(tot_bytes) / len(tot_bytes)
         lines += ["", f"mean DRAM bytes per launch: {mean:.4e}"]
         open(os.path.join(ROOT, "profiles", f"{tag}_ncu_{name}.md"), "w").write(
@@ -83,8 +94,11 @@ def main():
         if "_full_" in name:
             mode = name.rsplit("_", 1)[-1]
             traffic[f"{mode}_65536x512"] = mean
+            pipes[f"{mode}_65536x512"] = {"source": f"profiles/{tag}_ncu_{name}.md",
+                                          "per_launch": pipe_rows}
         print(name, mean)
     json.dump(traffic, open(tfile, "w"), indent=1)
+    json.dump(pipes, open(pfile, "w"), indent=1)
 
 
 if __name__ == "__main__":
