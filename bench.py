@@ -10,10 +10,11 @@ points PER GPU (radial slabs of a (65536 N) x 512 grid), extremal-Kerr
 s=-2 m=2 sign structure, WENO5, SSP-RK3, mixed precision (fp32 WENO
 weights, fp64 state) as the headline and fp64 beside it.  Inputs are larger
 than L2 (state 1.07 GB per register, coefficients 2.4 GB), so no explicit
-L2 flush is needed between steps.  Coefficients are synthetic
-(paper_2010_04760_b200/synthetic.py): the reference's own setup would take
-~3.5 min of serial double-double work at this size and is host setup, not
-the measured path.
+L2 flush is needed between steps.  Coefficients are the reference's own
+extremal-Kerr planes, assembled on the GPU by hwg_assemble_coefficients
+(the reference's generated wave_op_coeffs kernels in double-double,
+paper_2010_04760_b200/planes.py; untimed setup, ~3.5 min of serial host
+work in the reference); the initial state is a Gaussian pulse.
 
 One JSON line on rank 0.  See DESIGN.md §5 for the roofline bookkeeping.
 """
@@ -232,7 +233,9 @@ def run_reference(args):
             "steps": K, "steps_requested": args.steps, "warmup": W,
             "ms_per_step": 1000 * wall / max(K, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "dd state, fp64 weights", "data": "synthetic",
+            "dtype": "dd state, fp64 weights",
+            "data": "the reference's own make_grid + assemble_coefficients planes (C5 physics) "
+                    "and initial_data (ell=2 Gaussian)",
             "config": {"workload": f"C5 shape {nrho}x{ntheta} per GPU, C5 physics (a=1, s=-2, "
                                    f"m=2), WENO5, SSP-RK3 (the B200 arm's workload)",
                        "scheme": "weno5", "stepper": "ssprk33", "mode": "reference mixed",
@@ -358,14 +361,23 @@ def time_mode(args, mode, prob, world, rank, dev, torch, dist, steps=None, warmu
                    kern_ms=kern_ms, P=P, dt=dt, K=K, halo=halo, runner=runner)
 
 
-def sustained_mode(g, args, prob, dt, torch, clocks_cls, dev, warm_s=1.0, timed_s=2.5):
+def sustained_mode(g, args, prob, dt, torch, clocks_cls, dev, warm_s=1.0, timed_s=2.5,
+                   tau_chunk=20.0):
     """The headline tier under sustained load: whole SSP-RK3 steps replayed
     back to back (hwg_launch_steps, CUDA graphs) for >= warm_s untimed, then
     >= timed_s timed with CUDA events and its own clock record (the 20-step
-    burst sits inside the power-cap transient)."""
+    burst sits inside the power-cap transient).  The extremal
+    Kerr m=2 pulse grows by ~e per 3 units of tau on the fast tiers as in the
+    reference (tools/probe_growth.py), so a small grid, which needs ~10^5 steps
+    to fill the window, restarts from the initial state every tau_chunk
+    (a host set_state between timed chunks, outside the events; the C5 grid
+    never needs one)."""
     stream = torch.cuda.current_stream()
     g.set_stream(stream.cuda_stream)  # e2e_mode may have moved the handle to its own stream
     P = prob["nrho"] * prob["ntheta"]
+    from paper_2010_04760_b200 import synthetic
+    u0 = synthetic.initial_state(prob)
+    g.set_state(u0)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     g.launch_steps("ssprk33", dt, 0, 20)
     e0.record(stream)
@@ -375,22 +387,43 @@ def sustained_mode(g, args, prob, dt, torch, clocks_cls, dev, warm_s=1.0, timed_
     per = max(e0.elapsed_time(e1) / 20.0, 1e-3)
     nw = min(100000, max(20, int(warm_s * 1e3 / per)))
     nt = min(100000, max(20, int(timed_s * 1e3 / per)))
+    chunk = max(20, int(tau_chunk / dt))
+    state = {"step": 40, "restarts": 0}
+
+    def run(n, timed):
+        """n steps in chunks that stay within tau_chunk of a (re)start."""
+        ms = 0.0
+        while n > 0:
+            k = min(n, chunk)
+            if state["step"] + k > chunk:  # restart the pulse (untimed)
+                torch.cuda.synchronize()
+                g.set_state(u0)
+                state["step"] = 0
+                state["restarts"] += 1
+            if timed:
+                e0.record(stream)
+            g.launch_steps("ssprk33", dt, state["step"], k)
+            if timed:
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms += e0.elapsed_time(e1)
+                if g.status()[0]:
+                    raise RuntimeError("sustained run blew up")
+            state["step"] += k
+            n -= k
+        return ms
+
     ck = clocks_cls(dev)
     ck.start()
-    g.launch_steps("ssprk33", dt, 40, nw)
+    run(nw, False)
     ck.mark()
-    e0.record(stream)
-    g.launch_steps("ssprk33", dt, 40 + nw, nt)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms = run(nt, True)
     ck.mark()
     ck.stop()
-    ms = e0.elapsed_time(e1)
-    blown, _ = g.status()
-    if blown:
-        raise RuntimeError("sustained run blew up")
+    restarts = state["restarts"]
     return {"value": P * 3 * nt / (ms / 1e3), "ms_per_step": ms / nt, "steps": nt,
-            "warm_steps": nw, "timed_s": ms / 1e3, "clocks": ck.summary()}
+            "warm_steps": nw, "timed_s": ms / 1e3, "restarts": restarts,
+            "clocks": ck.summary()}
 
 
 def _e2e_job(g, u, out, dt, q, runner=None):
@@ -530,6 +563,13 @@ CONFIG_SHAPES = [
     ("C3 16384x128 weno5 f64", 16384, 128, "weno5", "f64"),
     ("C4 4096x128 fd6ko", 4096, 128, "fd6ko", "mixed"),
 ]
+# their physics: the reference's planes assembled on the GPU
+CONFIG_PHYSICS = {
+    "C1": dict(a=0.0, spin=0, mmode=0),
+    "C2": dict(a=1.0, spin=-2, mmode=2),
+    "C3": dict(a=0.9, spin=-2, mmode=0),
+    "C4": dict(a=1.0, spin=-2, mmode=2),
+}
 
 
 def config_rates(torch):
@@ -538,11 +578,11 @@ def config_rates(torch):
     (hwg_launch_steps) for ~50 ms after 5 warm-up steps.  C1-C4 fit in the
     126 MB L2 (no flush: the point is the resident-grid rate) and are
     launch/latency bound rather than HBM bound."""
-    from paper_2010_04760_b200 import hwgpu, synthetic
+    from paper_2010_04760_b200 import hwgpu, planes, synthetic
     out = {}
     stream = torch.cuda.current_stream()
     for label, n, nt, sch, mode in CONFIG_SHAPES:
-        prob = synthetic.problem(n, nt)
+        prob = planes.problem(n, nt, **CONFIG_PHYSICS[label[:2]])
         g = hwgpu.GpuEvolution(n, nt, prob["drho"], prob["dtheta"], prob["parity"],
                                prob["coef"], prob["cotth"], hwgpu.SchemeSpec(sch, mode))
         g.set_stream(stream.cuda_stream)
@@ -626,11 +666,19 @@ def run_b200(args):
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
-    from paper_2010_04760_b200 import slabs, synthetic
+    from paper_2010_04760_b200 import planes, slabs
 
     ng = args.nrho * world
     off, cnt = slabs.partition(ng, world)[rank]
-    prob = synthetic.problem(cnt, args.ntheta, rho_offset=off, nrho_global=ng)
+    t0 = time.perf_counter()
+    prob = planes.problem(cnt, args.ntheta, rho_offset=off, nrho_global=ng, device=dev)
+    setup_s = time.perf_counter() - t0
+    log(f"coefficient planes assembled on the GPU in {setup_s:.2f} s")
+    if world > 1:  # one dt for all slabs: the whole grid's max speed
+        ms = torch.tensor([prob["max_speed"]], dtype=torch.float64,
+                          device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        prob["max_speed"] = float(ms.item())
     clocks = ClockSampler(dev)
     clocks.start()
     results = {}
@@ -720,9 +768,10 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": head["total_ms"] / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 state, fp32 WENO weights" if args.mode == "mixed" else "f64",
-        "data": "synthetic (BASELINE shape; synthetic coefficient planes with the reference's "
-                "structure, Gaussian pulse; on the reference's real C5 planes the same kernels "
-                "run at 1.016x this rate: tools/real_planes_bench.py, profiles/r02_real_planes.json)",
+        "data": "the reference's extremal-Kerr (a=M, s=-2, m=2) coefficient planes on the "
+                f"BASELINE C5 grid, assembled on the GPU in {setup_s:.2f} s by the reference's "
+                "generated wave_op_coeffs kernels in double-double (hwg_assemble_coefficients, "
+                "fp64 grid); synthetic initial state (Gaussian pulse)",
         "config": {"workload": f"C5 shape {args.nrho}x{args.ntheta} per GPU (radial slabs of "
                                f"{args.nrho * world}x{args.ntheta}), WENO5 {args.mode}, SSP-RK3",
                    "grid_points_per_gpu": head["P"], "stages_per_step": 3,

@@ -51,6 +51,49 @@ inline void check(int rc, const hwg_solver* s) {
 
 enum class Tier { exact, fast };
 
+// assemble_coefficients (proj/src/geometry.cpp:118-168) on the GPU
+// (SURVEY.md §8f-2): every CoefficientSet plane and max_speed bitwise equal to
+// the reference's serial loop (hwg_assemble_coefficients evaluates the
+// reference's own generated wave_op_coeffs<DDReal> in double-double, one
+// thread per point); cotth is the reference's host loop (geometry.cpp:
+// 131-132).  The hyperbolicity error is the reference's runtime_error.
+//
+//   hweno::CoefficientSet cs = assemble_coefficients(g, p);                // reference
+//   hweno::CoefficientSet cs = hweno_gpu::assemble_coefficients_device(g, p);  // GPU
+inline hweno::CoefficientSet assemble_coefficients_device(const hweno::Grid& g,
+                                                          const hweno::PhysicalParams& p,
+                                                          int device = 0) {
+  using hweno::WorkReal;
+  static_assert(sizeof(WorkReal) == 2 * sizeof(double), "DDReal is {double hi, lo}");
+  hweno::CoefficientSet c;
+  c.nrho = g.nrho;
+  c.ntheta = g.ntheta;
+  const size_t n = size_t(g.nrho) * g.ntheta;
+  std::vector<WorkReal>* planes[14] = {&c.b,     &c.lam,   &c.w_re,  &c.w_im,  &c.bt_re,
+                                       &c.bt_im, &c.c_re,  &c.c_im,  &c.ath,   &c.p_mix,
+                                       &c.r_rad, &c.br_re, &c.br_im, &c.bprime};
+  double* out[14];
+  for (int q = 0; q < 14; ++q) {
+    planes[q]->resize(n);
+    out[q] = reinterpret_cast<double*>(planes[q]->data());
+  }
+  c.cotth.resize(g.ntheta);
+  for (int k = 0; k < g.ntheta; ++k) c.cotth[k] = g.costh[k] / g.sinth[k];
+  const double M[2] = {p.M.hi, p.M.lo}, a[2] = {p.a.hi, p.a.lo}, S[2] = {p.S.hi, p.S.lo};
+  double vmax[2];
+  int bad[2];
+  const int rc = hwg_assemble_coefficients(
+      device, reinterpret_cast<const double*>(g.rho.data()), g.nrho,
+      reinterpret_cast<const double*>(g.costh.data()), g.ntheta, M, a, S, p.spin, p.mmode, out,
+      vmax, bad);
+  if (rc == HWG_ERUNTIME && bad[0] >= 0)  // geometry.cpp:146-149, its message
+    throw std::runtime_error("hyperbolicity violated at rho=" + std::to_string(g.rho[bad[0]].hi) +
+                             " theta=" + std::to_string(g.theta[bad[1]].hi));
+  check(rc, nullptr);
+  c.max_speed = WorkReal(vmax[0], vmax[1]);
+  return c;
+}
+
 class GpuEvolutionRhs {
  public:
   GpuEvolutionRhs(const hweno::Grid& g, const hweno::CoefficientSet& cs,

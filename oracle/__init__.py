@@ -65,6 +65,10 @@ def ref_lib():
         lib.ref_info.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_longlong)]
         lib.ref_coeffs.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp]
         lib.ref_cotth_lo.argtypes = [C.c_void_p, _dp]
+        lib.ref_grid_dd.argtypes = [C.c_void_p, _dp, _dp]
+        lib.ref_coeffs_all_dd.argtypes = [C.c_void_p, _dp, _dp]
+        lib.ref_wave_op_coeffs.argtypes = [C.c_int, _dp, C.POINTER(C.c_int), _dp]
+        lib.ref_rat.argtypes = [C.c_longlong, C.c_longlong, _dp]
         lib.ref_initial_data.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double,
                                          C.c_double, _dp]
         lib.ref_rhs.argtypes = [C.c_void_p, _dp, _dp]
@@ -200,6 +204,21 @@ class RefSolver:
         """(9, ntheta, nrho) view, plane order b, lam, w_re, w_im, bt_re, bt_im, c_re, c_im, ath."""
         return self.coef.reshape(9, self.ntheta, self.nrho)
 
+    def grid_dd(self):
+        """Grid::rho (nrho, 2) and Grid::costh (ntheta, 2) as DD {hi, lo} pairs."""
+        rho = np.zeros(2 * self.nrho)
+        cth = np.zeros(2 * self.ntheta)
+        _chk(ref_lib().ref_grid_dd(self.h, _ptr(rho), _ptr(cth)))
+        return rho.reshape(-1, 2), cth.reshape(-1, 2)
+
+    def coeffs_all_dd(self):
+        """All 14 CoefficientSet planes as (14, ntheta, nrho, 2) DD pairs, and max_speed (2,)."""
+        P = self.nrho * self.ntheta
+        planes = np.zeros(14 * P * 2)
+        ms = np.zeros(2)
+        _chk(ref_lib().ref_coeffs_all_dd(self.h, _ptr(planes), _ptr(ms)))
+        return planes.reshape(14, self.ntheta, self.nrho, 2), ms
+
     def initial_data(self, phys: Physics | None = None):
         p = phys or self.phys
         dd = np.zeros(2 * self.state_size)
@@ -299,6 +318,24 @@ def ref_weno5_row(u_hi, drho, eps, mode, minus):
     _chk(ref_lib().ref_weno5_row(_ptr(dd), n, drho, eps, 0 if mode == "full" else 1,
                                  int(minus), _ptr(out)))
     return out[0::2].copy(), out[1::2].copy()
+
+
+def ref_wave_op_coeffs(inp, spin_mmode):
+    """wave_op_coeffs<DDReal> at n points: inp (n, 5, 2) DD {rho, cth, M, a, S},
+    spin_mmode (n, 2) int -> (n, 11, 2) DD."""
+    x = np.ascontiguousarray(inp, dtype=np.float64).reshape(-1)
+    sm = np.ascontiguousarray(spin_mmode, dtype=np.int32).reshape(-1)
+    n = sm.size // 2
+    out = np.zeros(22 * n)
+    _chk(ref_lib().ref_wave_op_coeffs(n, _ptr(x), sm.ctypes.data_as(C.POINTER(C.c_int)), _ptr(out)))
+    return out.reshape(n, 11, 2)
+
+
+def ref_rat(p: int, q: int) -> np.ndarray:
+    """DDReal(p) / DDReal(q) as a (2,) {hi, lo} pair."""
+    out = np.zeros(2)
+    _chk(ref_lib().ref_rat(p, q, _ptr(out)))
+    return out
 
 
 def ref_weno5_weights(a5, eps, mode):

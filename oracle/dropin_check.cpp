@@ -139,20 +139,30 @@ int main(int argc, char** argv) {
     auto t1 = std::chrono::steady_clock::now();
     CoefficientSet b = hweno_gpu::assemble_coefficients_parallel(g, p);
     auto t2 = std::chrono::steady_clock::now();
-    const std::vector<WorkReal>* pa[14] = {&a.b, &a.lam, &a.w_re, &a.w_im, &a.bt_re, &a.bt_im, &a.c_re,
-                                           &a.c_im, &a.ath, &a.p_mix, &a.r_rad, &a.br_re, &a.br_im, &a.bprime};
-    const std::vector<WorkReal>* pb[14] = {&b.b, &b.lam, &b.w_re, &b.w_im, &b.bt_re, &b.bt_im, &b.c_re,
-                                           &b.c_im, &b.ath, &b.p_mix, &b.r_rad, &b.br_re, &b.br_im, &b.bprime};
-    long diff = 0;
-    for (int q = 0; q < 14; ++q)
-      diff += std::memcmp(pa[q]->data(), pb[q]->data(), pa[q]->size() * sizeof(WorkReal)) != 0;
-    diff += std::memcmp(a.cotth.data(), b.cotth.data(), a.cotth.size() * sizeof(WorkReal)) != 0;
-    diff += !(a.max_speed == b.max_speed);
+    CoefficientSet d = hweno_gpu::assemble_coefficients_device(g, p);
+    auto t3 = std::chrono::steady_clock::now();
+    auto ndiff = [&](const CoefficientSet& x) {
+      const std::vector<WorkReal>* pa[14] = {&a.b, &a.lam, &a.w_re, &a.w_im, &a.bt_re, &a.bt_im, &a.c_re,
+                                             &a.c_im, &a.ath, &a.p_mix, &a.r_rad, &a.br_re, &a.br_im, &a.bprime};
+      const std::vector<WorkReal>* pb[14] = {&x.b, &x.lam, &x.w_re, &x.w_im, &x.bt_re, &x.bt_im, &x.c_re,
+                                             &x.c_im, &x.ath, &x.p_mix, &x.r_rad, &x.br_re, &x.br_im, &x.bprime};
+      long diff = 0;
+      for (int q = 0; q < 14; ++q)
+        diff += std::memcmp(pa[q]->data(), pb[q]->data(), pa[q]->size() * sizeof(WorkReal)) != 0;
+      diff += std::memcmp(a.cotth.data(), x.cotth.data(), a.cotth.size() * sizeof(WorkReal)) != 0;
+      diff += std::memcmp(&a.max_speed, &x.max_speed, sizeof(WorkReal)) != 0;
+      return diff;
+    };
+    const long diff = ndiff(b), ddiff = ndiff(d);
     const double ts = std::chrono::duration<double>(t1 - t0).count();
     const double tp = std::chrono::duration<double>(t2 - t1).count();
+    const double td = std::chrono::duration<double>(t3 - t2).count();
     std::printf("coefficients 2048x64: serial %.3f s, threaded %.3f s (%.1fx), planes differing %ld %s\n",
                 ts, tp, ts / tp, diff, diff == 0 ? "OK" : "FAIL");
+    std::printf("coefficients 2048x64 on the GPU: %.3f s (%.1fx serial), planes differing %ld %s\n", td,
+                ts / td, ddiff, ddiff == 0 ? "OK" : "FAIL");
     bad += diff != 0;
+    bad += ddiff != 0;
   }
   // ---- §8f-3: checkpoint / restart through the GPU state (test_io.cpp:320-360)
   {

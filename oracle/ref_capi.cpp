@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "hweno/angular.hpp"
+#include "hweno/coeff_kernels.hpp"
 #include "hweno/diagnostics.hpp"
 #include "hweno/evolve.hpp"
 #include "hweno/geometry.hpp"
@@ -171,6 +172,71 @@ int ref_coeffs(void* hv, double* planes, double* lo, double* cotth,
       for (int j = 0; j < h->g.nrho; ++j) rho[j] = h->g.rho[j].hi;
     if (theta)
       for (int k = 0; k < h->g.ntheta; ++k) theta[k] = h->g.theta[k].hi;
+  });
+}
+
+// Grid::rho / Grid::costh as DD pairs (inputs of hwg_assemble_coefficients)
+int ref_grid_dd(void* hv, double* rho_dd, double* costh_dd) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    for (int j = 0; j < h->g.nrho; ++j) {
+      rho_dd[2 * j] = h->g.rho[j].hi;
+      rho_dd[2 * j + 1] = h->g.rho[j].lo;
+    }
+    for (int k = 0; k < h->g.ntheta; ++k) {
+      costh_dd[2 * k] = h->g.costh[k].hi;
+      costh_dd[2 * k + 1] = h->g.costh[k].lo;
+    }
+  });
+}
+
+// all 14 CoefficientSet planes (geometry.hpp:73-90 order: b, lam, w_re,
+// w_im, bt_re, bt_im, c_re, c_im, ath, p_mix, r_rad, br_re, br_im, bprime)
+// as DD pairs, 14 x P x 2 doubles, and max_speed
+int ref_coeffs_all_dd(void* hv, double* planes_dd, double* max_speed_dd) {
+  auto* h = static_cast<RefHandle*>(hv);
+  return guarded([&] {
+    const std::vector<WorkReal>* src[14] = {
+        &h->cs.b,     &h->cs.lam,   &h->cs.w_re,  &h->cs.w_im,  &h->cs.bt_re,
+        &h->cs.bt_im, &h->cs.c_re,  &h->cs.c_im,  &h->cs.ath,   &h->cs.p_mix,
+        &h->cs.r_rad, &h->cs.br_re, &h->cs.br_im, &h->cs.bprime};
+    const size_t P = size_t(h->g.nrho) * h->g.ntheta;
+    for (int q = 0; q < 14; ++q)
+      for (size_t i = 0; i < P; ++i) {
+        planes_dd[2 * (q * P + i)] = (*src[q])[i].hi;
+        planes_dd[2 * (q * P + i) + 1] = (*src[q])[i].lo;
+      }
+    max_speed_dd[0] = h->cs.max_speed.hi;
+    max_speed_dd[1] = h->cs.max_speed.lo;
+  });
+}
+
+// wave_op_coeffs<DDReal> (coeff_kernels.hpp:661-666) at n points:
+// in = n x {rho, cth, M, a, S} DD pairs, sm = n x {spin, mmode},
+// out = n x 11 DD pairs (a_tr a_rr bt_re bt_im br_re br_im c_re c_im a_th da_tr da_rr)
+int ref_wave_op_coeffs(int n, const double* in, const int* sm, double* out) {
+  return guarded([&] {
+    for (int i = 0; i < n; ++i) {
+      const double* x = in + 10 * i;
+      auto w = wave_op_coeffs<WorkReal>(DDReal(x[0], x[1]), DDReal(x[2], x[3]), DDReal(x[4], x[5]),
+                                        DDReal(x[6], x[7]), DDReal(x[8], x[9]), sm[2 * i],
+                                        sm[2 * i + 1]);
+      const WorkReal v[11] = {w.a_tr, w.a_rr, w.bt_re, w.bt_im, w.br_re, w.br_im,
+                              w.c_re, w.c_im, w.a_th,  w.da_tr, w.da_rr};
+      for (int q = 0; q < 11; ++q) {
+        out[22 * i + 2 * q] = v[q].hi;
+        out[22 * i + 2 * q + 1] = v[q].lo;
+      }
+    }
+  });
+}
+
+// DDReal(p) / DDReal(q) (the reference tests' rat(), test_geometry.cpp)
+int ref_rat(long long p, long long q, double* out_dd) {
+  return guarded([&] {
+    const DDReal r = DDReal(p) / DDReal(q);
+    out_dd[0] = r.hi;
+    out_dd[1] = r.lo;
   });
 }
 

@@ -73,6 +73,28 @@ HWG_HD dd operator*(dd a, double b) {
   return {p1, p2};
 }
 HWG_HD dd D(double x) { return {x, 0.0}; }
+// precision.hpp:103-112 operator/(DDReal, DDReal) with IEEE divisions (the
+// stage kernels use their own branch-free form, hwg_dd.cuh div_dd)
+HWG_HD dd dd_div_ieee(dd a, dd b) {
+  const double q1 = a.hi / b.hi;
+  dd r = a - b * q1;
+  const double q2 = r.hi / b.hi;
+  r = r - b * q2;
+  const double q3 = r.hi / b.hi;
+  double s2;
+  const double s1 = dd_qts(q1, q2, s2);
+  return dd{s1, s2} + q3;
+}
+// precision.hpp sqrt(DDReal): one Karp-Markstein correction of the double
+// estimate
+HWG_HD dd dd_sqrt(dd a) {
+  if (a.hi == 0.0 && a.lo == 0.0) return D(0.0);
+  if (a.hi < 0.0) return D(nan(""));
+  const double x = 1.0 / sqrt(a.hi);
+  const double ax = a.hi * x;
+  const dd d = a - D(ax) * D(ax);
+  return D(ax) + d.hi * (x * 0.5);
+}
 
 
 // ---- strength reductions (bitwise equal to the reference forms)

@@ -3,6 +3,8 @@
 // parallelises; hwg_solver.cu only sees these entry points.
 #pragma once
 
+#include <string>
+
 #include "hwg_dd.cuh"
 #include "hwg_kernels.cuh"
 
@@ -41,4 +43,6 @@ struct EmuArgs {
 // capacity: co-resident blocks of the emulation kernel on this device
 cudaError_t launch_peer_emu(const EmuArgs& m, int scheme, int mode, int blocks,
                             cudaStream_t stream, int* capacity);
+// hwg_last_error(NULL) for the handle-less entry points (coefficient assembly)
+void set_global_error(const std::string& msg);
 }  // namespace hwg

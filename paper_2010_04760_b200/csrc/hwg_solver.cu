@@ -23,6 +23,12 @@
 using namespace hwg;
 
 namespace {
+thread_local std::string g_create_err;
+}  // namespace
+// hwg_last_error(NULL) of the handle-less entry points (hwg_coef.cu)
+void hwg::set_global_error(const std::string& msg) { g_create_err = msg; }
+
+namespace {
 // NVTX range over a C-ABI entry point (no-op unless a profiler is attached)
 struct NvtxRange {
   explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
@@ -31,7 +37,6 @@ struct NvtxRange {
 }  // namespace
 
 namespace {
-thread_local std::string g_create_err;
 // CUDA-graph cache entries per handle (least recently used goes first)
 constexpr size_t kMaxGraphs = 8;
 // fused halo push: minimum rows per rho range (max(IL, R, halo) over the schemes)

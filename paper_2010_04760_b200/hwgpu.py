@@ -104,6 +104,15 @@ _lib.hwg_peer_stats.argtypes = [_vp, C.POINTER(C.c_longlong)]
 _lib.hwg_peer_emulate_steps.argtypes = [C.POINTER(_vp), C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_longlong, C.c_longlong, C.c_longlong]
 
+_dpp = C.POINTER(_dp)
+_lib.hwg_assemble_coefficients.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_int, _dp, _dp, _dp,
+                                           C.c_int, C.c_int, _dpp, _dp, C.POINTER(C.c_int)]
+_lib.hwg_assemble_coefficients_split.argtypes = [C.c_int, _dp, C.c_int, _dp, C.c_int, _dp, _dp,
+                                                 _dp, C.c_int, C.c_int, _dpp, _dpp, _dp,
+                                                 C.POINTER(C.c_int)]
+_lib.hwg_wave_op_coeffs.argtypes = [C.c_int, C.c_int, _dp, C.POINTER(C.c_int), _dp]
+_lib.hwg_have_coefficient_kernels.argtypes = []
+
 EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg_set_stream", "hwg_set_state_dd",
             "hwg_get_state_dd", "hwg_set_state", "hwg_get_state", "hwg_rhs", "hwg_rhs_dd",
             "hwg_advance", "hwg_set_observers", "hwg_observe", "hwg_launch_stage",
@@ -111,7 +120,9 @@ EXPORTED = ["hwg_create", "hwg_create_dd", "hwg_destroy", "hwg_last_error", "hwg
             "hwg_current_register", "hwg_status", "hwg_launch_info", "hwg_synchronize",
             "hwg_peer_export", "hwg_set_peers", "hwg_peer_prime", "hwg_abort_advance",
             "hwg_launch_stage_rows", "hwg_peer_stats", "hwg_peer_emulate_steps",
-            "hwg_selftest_division"]
+            "hwg_selftest_division", "hwg_assemble_coefficients",
+            "hwg_assemble_coefficients_split", "hwg_wave_op_coeffs",
+            "hwg_have_coefficient_kernels"]
 
 
 class HwgError(RuntimeError):
@@ -121,6 +132,94 @@ class HwgError(RuntimeError):
 def _p(a: np.ndarray):
     assert a.dtype == np.float64 and a.flags.c_contiguous
     return a.ctypes.data_as(_dp)
+
+
+# CoefficientSet planes in their order (proj/include/hweno/geometry.hpp:73-90)
+COEF_PLANES = ("b", "lam", "w_re", "w_im", "bt_re", "bt_im", "c_re", "c_im", "ath", "p_mix",
+               "r_rad", "br_re", "br_im", "bprime")
+
+
+def _dd2(x) -> np.ndarray:
+    """A DD scalar as a (2,) {hi, lo} array (a float is {x, 0})."""
+    a = np.zeros(2)
+    a[:] = x if np.ndim(x) else (float(x), 0.0)
+    return a
+
+
+def _coef_err(rc: int, bad=None):
+    msg = _lib.hwg_last_error(None).decode()
+    if rc == 2:
+        raise ValueError(msg)
+    err = HwgError(msg)
+    err.bad_jk = None if bad is None else (bad[0], bad[1])
+    raise err
+
+
+def assemble_coefficients(rho_dd, costh_dd, M=1.0, a=0.0, S=20.0, spin=0, mmode=0,
+                          planes=COEF_PLANES, layout="dd", device: int = 0, into=None):
+    """assemble_coefficients (proj/src/geometry.cpp:118-168) on the GPU:
+    rho_dd (nrho, 2) and costh_dd (ntheta, 2) DD grids (Grid::rho,
+    Grid::costh), M / a / S floats or (hi, lo) pairs.
+    layout 'dd'   -> {name: (ntheta, nrho, 2) DD pairs}  (CoefficientSet storage)
+    layout 'split'-> {name: ((ntheta, nrho) hi, (ntheta, nrho) lo)}
+    layout 'hi'   -> {name: (ntheta, nrho) hi}
+    plus 'max_speed' -> (2,) DD.  layout 'hi' with `into` (len(planes),
+    ntheta, nrho) C-contiguous fp64: written in place (no copies).  Raises
+    HwgError (with .bad_jk) where the reference throws 'hyperbolicity
+    violated'."""
+    rho = np.ascontiguousarray(rho_dd, dtype=np.float64).reshape(-1, 2)
+    cth = np.ascontiguousarray(costh_dd, dtype=np.float64).reshape(-1, 2)
+    nrho, nt = rho.shape[0], cth.shape[0]
+    want = set(planes)
+    unknown = want - set(COEF_PLANES)
+    if unknown:
+        raise ValueError(f"unknown planes {sorted(unknown)}")
+    ms = np.zeros(2)
+    bad = (C.c_int * 2)()
+    out, ptrs, lptrs = {}, (_dp * 14)(), (_dp * 14)()
+    for q, name in enumerate(COEF_PLANES):
+        if name not in want:
+            continue
+        if layout == "dd":
+            out[name] = np.empty((nt, nrho, 2))
+            ptrs[q] = _p(out[name])
+        elif layout in ("split", "hi"):
+            hi = np.empty((nt, nrho)) if into is None else into[list(planes).index(name)]
+            assert hi.shape == (nt, nrho) and hi.dtype == np.float64 and hi.flags.c_contiguous
+            ptrs[q] = _p(hi)
+            if layout == "split":
+                lo = np.empty((nt, nrho))
+                lptrs[q] = _p(lo)
+                out[name] = (hi, lo)
+            else:
+                out[name] = hi
+        else:
+            raise ValueError(f"layout {layout!r}")
+    args = (device, _p(rho), nrho, _p(cth), nt, _p(_dd2(M)), _p(_dd2(a)), _p(_dd2(S)),
+            int(spin), int(mmode))
+    if layout == "dd":
+        rc = _lib.hwg_assemble_coefficients(*args, ptrs, _p(ms), bad)
+    else:
+        rc = _lib.hwg_assemble_coefficients_split(*args, ptrs, lptrs, _p(ms), bad)
+    if rc != 0:
+        _coef_err(rc, bad)
+    out["max_speed"] = ms
+    return out
+
+
+def wave_op_coeffs(inp, spin_mmode, device: int = 0) -> np.ndarray:
+    """wave_op_coeffs<DDReal> (coeff_kernels.hpp:661-666) on the GPU at n
+    points: inp (n, 5, 2) DD {rho, cth, M, a, S}, spin_mmode (n, 2) ->
+    (n, 11, 2) DD {a_tr, a_rr, bt_re, bt_im, br_re, br_im, c_re, c_im, a_th,
+    da_tr, da_rr}."""
+    x = np.ascontiguousarray(inp, dtype=np.float64).reshape(-1)
+    sm = np.ascontiguousarray(spin_mmode, dtype=np.int32).reshape(-1)
+    n = sm.size // 2
+    out = np.zeros((n, 11, 2))
+    rc = _lib.hwg_wave_op_coeffs(device, n, _p(x), sm.ctypes.data_as(C.POINTER(C.c_int)), _p(out))
+    if rc != 0:
+        _coef_err(rc)
+    return out
 
 
 @dataclass

@@ -19,7 +19,7 @@ def pytest_configure(config):
 
 def golden_cases():
     names = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
-    return [n for n in names if not n.startswith(("c1_", "c2_", "c2desk_", "tail_"))]
+    return [n for n in names if not n.startswith(("c1_", "c2_", "c2desk_", "tail_", "coef_"))]
 
 
 def load_golden(name):
