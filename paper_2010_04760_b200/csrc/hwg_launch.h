@@ -20,6 +20,9 @@ void init_attributes_fast();
 void launch_stage_dd(const StageArgsDD& a, int scheme, int mode, int epi, int blocks, int wpb,
                      cudaStream_t stream);
 cudaError_t occupancy_dd(int* blocks_per_sm);
+// warps per 32-column theta chunk of the DD stage kernel (1, or 2 in the
+// lane = (column, component) form)
+int dd_warps_per_chunk();
 // self-test of the DD tier's branch-free division vs IEEE division
 cudaError_t div_selftest(long long n, unsigned long long seed, long long* mismatches,
                          long long* guard_fails);

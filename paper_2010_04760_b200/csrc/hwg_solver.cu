@@ -968,7 +968,8 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
     // work units: one warp per (theta chunk, rho range)
     const int upb = kWarpsPerBlock;
     const long long target = (long long)nsm * std::max(occ, 1) * upb;
-    long long nr = std::max<long long>(1, target / s->nchunks);
+    const int wpc = ddm ? dd_warps_per_chunk() : 1;  // warps per theta chunk
+    long long nr = std::max<long long>(1, target / ((long long)s->nchunks * wpc));
     // rows per range: as few as 2 on tiny grids to fill the wave (the window
     // warm-up costs ~2 rows of work, so larger grids keep longer ranges)
     // (the double-double kernel's window set-up assumes ranges of >= 4 rows)
@@ -977,7 +978,7 @@ int create_impl(const hwg_desc* d, const double* coef, const double* coef_lo, co
     nr = std::min<long long>(nr, std::max(1, s->n / minrows));
     s->nranges = (int)nr;
     // small grids: fewer warps per block so the warps spread over all SMs
-    const long long units = nr * s->nchunks;
+    const long long units = nr * s->nchunks * wpc;
     s->wpb = upb;  // warps per block
     while (s->wpb > 1 && units / s->wpb < nsm) s->wpb /= 2;
     s->blocks = (int)((units + s->wpb - 1) / s->wpb);

@@ -29,6 +29,8 @@ void init_attributes_dd() {
   (void)done;
 }
 
+int dd_warps_per_chunk() { return kDDWarpsPerChunk; }
+
 cudaError_t occupancy_dd(int* occ) {
   init_attributes_dd();
   cudaError_t e = cudaFuncSetAttribute(stage_kernel_dd<WENO5, F64, EPI_RK3>,
