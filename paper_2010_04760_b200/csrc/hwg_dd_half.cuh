@@ -228,6 +228,36 @@ stage_kernel_dd(const StageArgsDD A) {
     // ---- phase 1 (evolve.cpp:88-122), this lane's component
     dd dps, dpi;
     if (SCH != FD6KO) {
+#ifdef HWG_DD_PAIR
+      // both interfaces of the row (Psi, always minus; pi in its orientation)
+      // in one call: two independent chains for the scheduler
+      const bool o = lam.hi < 0.0;  // split_ rule (evolve.cpp:22)
+      if (o != opi) {
+        if (!o && SCH == WENO5) {
+          dd xx[PW + 1];
+          xx[0] = row_or_ghost_h(xblk, h, lane, j - 3, rs, A.phys_lo, K);
+#pragma unroll
+          for (int m = 0; m < PW; ++m) xx[m + 1] = wpi[m];
+          fpi = iface_h<SCH, MODE, PL + 1>(xx, false, -1, A);
+        } else {
+          fpi = iface_h<SCH, MODE, PL>(wpi, o, -1, A);
+        }
+        opi = o;
+      }
+      constexpr int cs_ = SL, cp_ = PL;
+      const dd2 r = SCH == WENO5
+          ? iface_two_call<SCH, MODE>(wps[cs_ + 3], wps[cs_ + 2], wps[cs_ + 1], wps[cs_], wps[cs_ - 1],
+                                      o ? wpi[cp_ + 3] : wpi[cp_ - 2], o ? wpi[cp_ + 2] : wpi[cp_ - 1],
+                                      o ? wpi[cp_ + 1] : wpi[cp_], o ? wpi[cp_] : wpi[cp_ + 1],
+                                      o ? wpi[cp_ - 1] : wpi[cp_ + 2], A.kdev, A.eps_hi)
+          : iface_two_call<SCH, MODE>(wps[cs_ + 2], wps[cs_ + 1], wps[cs_], wps[cs_], wps[cs_],
+                                      o ? wpi[cp_ + 2] : wpi[cp_ - 1], o ? wpi[cp_ + 1] : wpi[cp_],
+                                      o ? wpi[cp_] : wpi[cp_ + 1], wpi[cp_], wpi[cp_], A.kdev, A.eps_hi);
+      dps = (r.re - fps) * K.inv_drho;
+      fps = r.re;
+      dpi = (r.im - fpi) * K.inv_drho;
+      fpi = r.im;
+#else
       const dd cs = iface_h<SCH, MODE, SL>(wps, true, 0, A);
       dps = (cs - fps) * K.inv_drho;
       fps = cs;
@@ -249,6 +279,7 @@ stage_kernel_dd(const StageArgsDD A) {
       else pp = iface_h<SCH, MODE, PL>(wpi, o, 0, A);
       dpi = (pp - fpi) * K.inv_drho;
       fpi = pp;
+#endif
     } else {
       // fd6_derivative (spatial.hpp:178-182)
       auto fd6 = [&](dd m3, dd m2, dd m1, dd p1, dd p2, dd p3) {
@@ -279,8 +310,8 @@ stage_kernel_dd(const StageArgsDD A) {
     __syncwarp();
     const dd m2 = trow[cc * 2 + comp], m1 = trow[(cc + 1) * 2 + comp];
     const dd p1 = trow[(cc + 3) * 2 + comp], p2 = trow[(cc + 4) * 2 + comp];
-    const dd d1 = (m2 - mul_c(m1, 8.0) + mul_c(p1, 8.0) - p2) * K.inv1;
-    const dd d2 = (-m2 + mul_c(m1, 16.0) - mul_c(ps, 30.0) + mul_c(p1, 16.0) - p2) * K.inv2;
+    const dd d1 = (m2 - mul_p2(m1, 8.0) + mul_p2(p1, 8.0) - p2) * K.inv1;
+    const dd d2 = (-m2 + mul_p2(m1, 16.0) - mul_c(ps, 30.0) + mul_p2(p1, 16.0) - p2) * K.inv2;
     const dd ang = d2 + cot * d1;
 
     // ---- phase 3 (evolve.cpp:149-167): Psi row f_c = pi_c - b dPsi_c; pi row
@@ -301,7 +332,7 @@ stage_kernel_dd(const StageArgsDD A) {
     if (SCH == FD6KO) {
       // ko8_dissipation (spatial.hpp:184-191), evolve.cpp:169-176
       auto ko8 = [&](dd u4m, dd u3m, dd u2m, dd u1m, dd u0, dd u1p, dd u2p, dd u3p, dd u4p) {
-        dd d8 = u4m + u4p - mul_c(u3m + u3p, 8.0) + mul_c(u2m + u2p, 28.0) -
+        dd d8 = u4m + u4p - mul_p2(u3m + u3p, 8.0) + mul_c(u2m + u2p, 28.0) -
                 mul_c(u1m + u1p, 56.0) + mul_c(u0, 70.0);
         return K.sigma * d8 / K.h256;
       };

@@ -61,7 +61,7 @@ int main(int argc, char** argv) {
   const long n = argc > 1 ? std::atol(argv[1]) : 4000000;
   Gen g(20260101);
   const double consts[] = {2, 3, 4, 5, 6, 7, 8, 9, 11, 16, 28, 30, 45, 56, 70, 0.25, 0.5};
-  long bad[4] = {0, 0, 0, 0}, tried[4] = {0, 0, 0, 0};
+  long bad[5] = {0, 0, 0, 0, 0}, tried[5] = {0, 0, 0, 0, 0};
   for (long i = 0; i < n; ++i) {
     // (1) mul_c(a, c) == DD(c) * a
     {
@@ -74,6 +74,17 @@ int main(int argc, char** argv) {
           if (bad[0]++ < 5)
             std::printf("mul_c a=(%a,%a) c=%a: %a %a vs %a %a\n", a.hi, a.lo, c, r1.hi, r1.lo, r2.hi, r2.lo);
         }
+      }
+    }
+    // (1b) mul_p2(a, c) == DD(c) * a for c = 2^k >= 1
+    {
+      const dd a = g.pair();
+      const double c = std::ldexp(1.0, (i & 1) ? (int)(i % 5) : (int)(g.r() % 200));
+      const dd r1 = hwg::mul_p2(a, c), r2 = dd{c, 0.0} * a;
+      if (finite(r2)) {
+        ++tried[4];
+        if (!same(r1, r2) && bad[4]++ < 5)
+          std::printf("mul_p2 a=(%a,%a) c=%a: %a %a vs %a %a\n", a.hi, a.lo, c, r1.hi, r1.lo, r2.hi, r2.lo);
       }
     }
     // (2) mul_x(b, x) == DD(x) * b
@@ -115,7 +126,7 @@ int main(int argc, char** argv) {
       }
     }
   }
-  std::printf("mul_c %ld/%ld  mul_x %ld/%ld  sum3_nn %ld/%ld  sum2_nn %ld/%ld mismatches\n", bad[0],
-              tried[0], bad[1], tried[1], bad[2], tried[2], bad[3], tried[3]);
-  return (bad[0] || bad[1] || bad[2] || bad[3]) ? 1 : 0;
+  std::printf("mul_c %ld/%ld  mul_p2 %ld/%ld  mul_x %ld/%ld  sum3_nn %ld/%ld  sum2_nn %ld/%ld mismatches\n",
+              bad[0], tried[0], bad[4], tried[4], bad[1], tried[1], bad[2], tried[2], bad[3], tried[3]);
+  return (bad[0] || bad[1] || bad[2] || bad[3] || bad[4]) ? 1 : 0;
 }
