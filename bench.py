@@ -640,6 +640,20 @@ def mode_record(m, r, peak):
                            "peak_source": src, "ops_per_point_stage": ops,
                            "achieved": ops * r["value"] if ops else None,
                            "frac": ops * r["value"] / fpk if ops else None}
+        # the measured ceiling of DD code at the kernel's occupancy (8 warps
+        # per SM): the WENO5 DD interface alone, register-resident, one chain
+        # per thread (tools/dd_peak.cu, profiles/r02_dd_peak.json)
+        try:
+            with open(os.path.join(ROOT, "profiles", "r02_dd_peak.json")) as f:
+                runs = json.load(f)["runs"]
+            name = "weno5_dd mixed" if m == "dd-mixed" else "weno5_dd full"
+            ceil = next(x["frac_of_dfma_peak"] for x in runs if x["kernel"] == name
+                        and x["warps_per_sm"] == 8 and x["chains_per_thread"] == 1)
+            rec["roofline"]["dd_interface_ceiling"] = ceil
+            if ops:
+                rec["roofline"]["frac_of_dd_ceiling"] = rec["roofline"]["frac"] / ceil
+        except Exception:
+            pass
         rec["frac_hbm_for_reference"] = rec.pop("frac")
     return rec
 

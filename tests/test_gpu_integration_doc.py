@@ -35,3 +35,24 @@ def test_integration_ctypes_snippet(cuda_ok):
     g.set_state(u0)
     g.launch_steps("ssprk33", env["dt"], 0, 1000)
     assert np.array_equal(env["u"][:, 2:-2, 4:-4], g.get_state()[:, 2:-2, 4:-4])
+
+
+def test_integration_assembly_snippet(cuda_ok):
+    """INTEGRATION.md §3's coefficient-assembly snippet (second python block),
+    executed as written on the reference's own DD grid: the planes are the
+    reference's assemble_coefficients output bit for bit."""
+    import ctypes as C
+    import oracle as O
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = re.findall(r"```python\n(.*?)```", text, re.S)[1]
+    ref = O.RefSolver(O.Physics(a=0.9, spin=-2, mmode=0), 256, 16, workers=4)
+    want, ms = ref.coeffs_all_dd()
+    rho, cth = ref.grid_dd()
+    env = dict(C=C, np=np, dp=C.POINTER(C.c_double),
+               lib=C.CDLL(os.path.join(ROOT, "paper_2010_04760_b200", "libhwgpu.so")),
+               nrho=256, ntheta=16, rho_dd=np.ascontiguousarray(rho), costh_dd=np.ascontiguousarray(cth))
+    exec(compile(code, "INTEGRATION.md", "exec"), env)
+    assert env["rc"] == 0
+    for q in range(14):
+        assert np.array_equal(env["planes"][q].view(np.int64), want[q].reshape(-1).view(np.int64)), q
+    assert np.array_equal(env["ms"].view(np.int64), ms.view(np.int64))
