@@ -582,7 +582,7 @@ def config_rates(torch):
     out = {}
     stream = torch.cuda.current_stream()
     for label, n, nt, sch, mode in CONFIG_SHAPES:
-        prob = planes.problem(n, nt, **CONFIG_PHYSICS[label[:2]])
+        prob = planes.problem_or_synthetic(n, nt, **CONFIG_PHYSICS[label[:2]])
         g = hwgpu.GpuEvolution(n, nt, prob["drho"], prob["dtheta"], prob["parity"],
                                prob["coef"], prob["cotth"], hwgpu.SchemeSpec(sch, mode))
         g.set_stream(stream.cuda_stream)
@@ -685,7 +685,7 @@ def run_b200(args):
     ng = args.nrho * world
     off, cnt = slabs.partition(ng, world)[rank]
     t0 = time.perf_counter()
-    prob = planes.problem(cnt, args.ntheta, rho_offset=off, nrho_global=ng, device=dev)
+    prob = planes.problem_or_synthetic(cnt, args.ntheta, rho_offset=off, nrho_global=ng, device=dev)
     setup_s = time.perf_counter() - t0
     log(f"coefficient planes assembled on the GPU in {setup_s:.2f} s")
     if world > 1:  # one dt for all slabs: the whole grid's max speed
@@ -782,10 +782,13 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": head["total_ms"] / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 state, fp32 WENO weights" if args.mode == "mixed" else "f64",
-        "data": "the reference's extremal-Kerr (a=M, s=-2, m=2) coefficient planes on the "
-                f"BASELINE C5 grid, assembled on the GPU in {setup_s:.2f} s by the reference's "
-                "generated wave_op_coeffs kernels in double-double (hwg_assemble_coefficients, "
-                "fp64 grid); synthetic initial state (Gaussian pulse)",
+        "data": ("the reference's extremal-Kerr (a=M, s=-2, m=2) coefficient planes on the "
+                 f"BASELINE C5 grid, assembled on the GPU in {setup_s:.2f} s by the reference's "
+                 "generated wave_op_coeffs kernels in double-double (hwg_assemble_coefficients, "
+                 "fp64 grid); synthetic initial state (Gaussian pulse)")
+                if prob["planes"] == "device-assembled" else
+                ("synthetic coefficient planes with the reference's sign structure (this "
+                 "libhwgpu.so was built without the reference headers); synthetic initial state"),
         "config": {"workload": f"C5 shape {args.nrho}x{args.ntheta} per GPU (radial slabs of "
                                f"{args.nrho * world}x{args.ntheta}), WENO5 {args.mode}, SSP-RK3",
                    "grid_points_per_gpu": head["P"], "stages_per_step": 3,

@@ -88,7 +88,7 @@ static __device__ __noinline__ dd row_or_ghost_h(const double2* xblk, int h, int
 #ifndef HWG_DD_MINB
 #define HWG_DD_MINB 3
 #endif
-template <int SCH, int MODE, int EPI>
+template <int SCH, int MODE, int EPI, bool INL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, HWG_DD_MINB)
 stage_kernel_dd(const StageArgsDD A) {
   if (A.flag != nullptr && *(volatile unsigned long long*)A.flag != 0ull) return;

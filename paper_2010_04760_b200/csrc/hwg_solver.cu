@@ -41,6 +41,9 @@ namespace {
 constexpr size_t kMaxGraphs = 8;
 // fused halo push: minimum rows per rho range (max(IL, R, halo) over the schemes)
 constexpr int kMinPeerRangeRows = 4;
+// DD tiers: rows per rho range from which the mixed tier's inlined row loop
+// is launched (hwg_stage_dd.cu, DDLauncher)
+constexpr int kDDInlineRows = 400;
 
 // Host double-double, an exact replica of the reference's DDReal operators
 // (proj/include/hweno/precision.hpp:16-115).  Like the reference, the host
@@ -406,6 +409,10 @@ StageArgsDD base_args_dd(const hwg_solver* s) {
   a.nranges = s->nranges;
   a.negpar = s->d.parity < 0 ? 1 : 0;
   a.eps_hi = s->eps.hi;  // demote(spec_.eps), evolve.cpp:79-80
+  // long rho ranges: the mixed tier's row-loop interfaces inlined (+5 % at
+  // 885 rows per range; -2..-9 % at 14-55 rows, profiles/r02_dd_ab2.txt)
+  a.inl = s->n >= kDDInlineRows * s->nranges ? 1 : 0;
+  if (const char* e = std::getenv("HWG_DD_INL")) a.inl = std::atoi(e);
   a.cot = reinterpret_cast<const dd*>(s->cot);
   a.coef = s->coef;
   a.flag = s->flag;

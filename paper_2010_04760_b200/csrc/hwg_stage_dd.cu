@@ -6,12 +6,23 @@ namespace hwg {
 namespace {
 template <int SCH, int MODE, int EPI>
 struct DDLauncher {
+  // the full tier has no INL instantiation (its interfaces always stay out of line)
+  static constexpr bool HAS_INL = MODE != F64;
   static void attr() {
-    cudaFuncSetAttribute(stage_kernel_dd<SCH, MODE, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)stage_smem_bytes_dd<EPI>());
+    cudaFuncSetAttribute(stage_kernel_dd<SCH, MODE, EPI, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_smem_bytes_dd<EPI>());
+    if constexpr (HAS_INL)
+      cudaFuncSetAttribute(stage_kernel_dd<SCH, MODE, EPI, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage_smem_bytes_dd<EPI>());
   }
   static void run(const StageArgsDD& a, int blocks, int wpb, cudaStream_t st) {
-    stage_kernel_dd<SCH, MODE, EPI><<<blocks, wpb * 32, stage_smem_bytes_dd<EPI>(wpb), st>>>(a);
+    if constexpr (HAS_INL) {
+      if (a.inl) {
+        stage_kernel_dd<SCH, MODE, EPI, true><<<blocks, wpb * 32, stage_smem_bytes_dd<EPI>(wpb), st>>>(a);
+        return;
+      }
+    }
+    stage_kernel_dd<SCH, MODE, EPI, false><<<blocks, wpb * 32, stage_smem_bytes_dd<EPI>(wpb), st>>>(a);
   }
 };
 }  // namespace
@@ -33,11 +44,11 @@ int dd_warps_per_chunk() { return kDDWarpsPerChunk; }
 
 cudaError_t occupancy_dd(int* occ) {
   init_attributes_dd();
-  cudaError_t e = cudaFuncSetAttribute(stage_kernel_dd<WENO5, F64, EPI_RK3>,
+  cudaError_t e = cudaFuncSetAttribute(stage_kernel_dd<WENO5, F64, EPI_RK3, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)stage_smem_bytes_dd<EPI_RK3>());
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, stage_kernel_dd<WENO5, F64, EPI_RK3>,
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, stage_kernel_dd<WENO5, F64, EPI_RK3, false>,
                                                        kWarpsPerBlock * 32,
                                                        stage_smem_bytes_dd<EPI_RK3>());
 }

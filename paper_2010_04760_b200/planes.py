@@ -38,6 +38,29 @@ def grid(nrho_global: int, ntheta: int, M=1.0, a=1.0, S=20.0):
     return rho, drho, dtheta, theta
 
 
+def available() -> bool:
+    """The library carries the reference's generated coefficient kernels
+    (built with the reference headers; hwg_have_coefficient_kernels)."""
+    from . import hwgpu
+    return bool(hwgpu._lib.hwg_have_coefficient_kernels())
+
+
+def problem_or_synthetic(nrho: int, ntheta: int, rho_offset: int = 0,
+                         nrho_global: int | None = None, **phys):
+    """problem() where the library has the coefficient kernels, else the
+    synthetic planes of the same shape (synthetic.problem) — benchmark input
+    data only; the dict's 'planes' key says which."""
+    if available():
+        p = problem(nrho, ntheta, rho_offset=rho_offset, nrho_global=nrho_global, **phys)
+        p["planes"] = "device-assembled"
+        return p
+    from . import synthetic
+    p = synthetic.problem(nrho, ntheta, rho_offset=rho_offset, nrho_global=nrho_global,
+                          **{k: v for k, v in phys.items() if k in ("a", "spin", "mmode", "S")})
+    p["planes"] = "synthetic"
+    return p
+
+
 def problem(nrho: int, ntheta: int, rho_offset: int = 0, nrho_global: int | None = None,
             M: float = 1.0, a: float = 1.0, spin: int = -2, mmode: int = 2, S: float = 20.0,
             device: int = 0):

@@ -10,7 +10,7 @@ for r in $(seq $R); do
   for L in libhwgpu.so "$@"; do
     for m in $MODES; do
       echo -n "$L r$r " >> $out
-      HWG_LIB=$PWD/paper_2010_04760_b200/$L timeout 300 python tools/prof_stage.py --mode $m --warmup ${WARM:-1} --steps ${STEPS:-3} >> $out 2>&1 || echo "$L $m failed" >> $out
+      HWG_LIB=$PWD/paper_2010_04760_b200/$L timeout 300 python tools/prof_stage.py --mode $m ${SHAPE:-} --warmup ${WARM:-1} --steps ${STEPS:-3} >> $out 2>&1 || echo "$L $m failed" >> $out
     done
   done
 done
