@@ -63,3 +63,22 @@ def test_assembly_without_gpu_fails_loudly():
     from paper_2010_04760_b200 import hwgpu
     with pytest.raises(hwgpu.HwgError):
         hwgpu.assemble_coefficients(np.zeros((16, 2)) + [[1.0, 0.0]], np.zeros((4, 2)), a=0.5)
+
+
+def test_bench_grid_is_the_reference_grid_in_fp64():
+    """planes.grid (the bench's fp64 grid for the device-assembled planes)
+    is make_grid's DD grid (geometry.cpp:68-116) rounded: rho within a few
+    ulps of the DD value's hi, the last point exactly S, cos(theta) within
+    4e-16 of Grid::costh (the fp64 theta's rounding, absolute)."""
+    import oracle as O
+    if not O.ref_available():
+        pytest.skip("reference library not built")
+    from paper_2010_04760_b200 import planes
+    for a, n, nt in ((1.0, 1024, 64), (0.9, 777, 33), (0.0, 256, 16)):
+        ref = O.RefSolver(O.Physics(a=a, spin=-2, mmode=2), n, nt, workers=4)
+        rho_dd, cth_dd = ref.grid_dd()
+        rho, drho, dtheta, theta = planes.grid(n, nt, a=a)
+        assert rho[-1] == 20.0 == rho_dd[-1, 0]
+        assert np.max(np.abs(rho - rho_dd[:, 0]) / np.spacing(rho_dd[:, 0])) <= 8
+        assert np.max(np.abs(np.cos(theta) - cth_dd[:, 0])) <= 4e-16
+        assert abs(drho - ref.drho) <= 2 * np.spacing(ref.drho)
