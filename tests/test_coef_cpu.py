@@ -44,16 +44,20 @@ def test_library_has_the_generated_kernels():
 
 
 def test_generated_header_only_adds_device_annotations():
-    """build.py's device copy of coeff_kernels.hpp differs from the
-    reference header only by the four __host__ __device__ annotations."""
+    """build.py's device copy of coeff_kernels.hpp (written to a temporary
+    directory for the compile only) differs from the reference header only by
+    the four __host__ __device__ annotations, and nothing reference-derived is
+    left in the repository tree."""
     from paper_2010_04760_b200 import build as b
     inc = b.ref_include()
     if inc is None:
         pytest.skip("reference headers absent")
-    gen = open(b.gen_coeff_header(inc)).read().split("\n", 1)[1]
+    gen = b.device_coeff_header_text(inc).split("\n", 1)[1]
     ref = open(os.path.join(inc, "hweno", "coeff_kernels.hpp")).read()
     assert gen.count("__host__ __device__ ") == 4
     assert gen.replace("__host__ __device__ ", "") == ref
+    for dirpath, _, files in os.walk(os.path.dirname(b.PKG)):
+        assert b.GEN_NAME not in files, dirpath
 
 
 def test_assembly_without_gpu_fails_loudly():
