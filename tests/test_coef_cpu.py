@@ -86,3 +86,14 @@ def test_bench_grid_is_the_reference_grid_in_fp64():
         assert np.max(np.abs(rho - rho_dd[:, 0]) / np.spacing(rho_dd[:, 0])) <= 8
         assert np.max(np.abs(np.cos(theta) - cth_dd[:, 0])) <= 4e-16
         assert abs(drho - ref.drho) <= 2 * np.spacing(ref.drho)
+
+
+def test_assembly_binding_validates_arguments():
+    """Argument errors surface before any device work (ValueError)."""
+    from paper_2010_04760_b200 import hwgpu
+    rho = np.zeros((16, 2)) + [[1.0, 0.0]]
+    cth = np.zeros((4, 2))
+    with pytest.raises(ValueError, match="unknown planes"):
+        hwgpu.assemble_coefficients(rho, cth, planes=("b", "nope"))
+    with pytest.raises(ValueError, match="layout"):
+        hwgpu.assemble_coefficients(rho, cth, layout="csv")

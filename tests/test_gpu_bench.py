@@ -41,6 +41,8 @@ def test_bench_json_line_small_grid(cuda_ok):
     assert su["value"] > 0 and su["timed_s"] >= 2.0 and "sm_mhz" in su["clocks"]
     ep = d["e2e_advance_production"]
     assert ep["hook_every"] > 1 and ep["hook_calls"] == 3 and ep["value"] > 0
+    # the bench runs on the reference's planes assembled on the GPU
+    assert "assembled on the GPU" in d["data"]
 
 
 def test_bench_two_ranks_control_flow_one_gpu(cuda_ok):
