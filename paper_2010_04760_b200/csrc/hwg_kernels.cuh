@@ -409,6 +409,14 @@ constexpr size_t stage_smem_bytes(int wpb = kWarpsPerBlock) {
   return stage_theta_offset<EPI>(wpb) + (size_t)wpb * 36 * 16;
 }
 
+// one lane of the (converged) warp, known to the compiler as a single lane
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -932,7 +940,10 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ri
     }
     // ---- release the slot and refill it S rows ahead
     __syncwarp();
-    if (lane == 0 && j + S < je) {
+    // one elected lane issues the next row's copies: with elect.sync the
+    // compiler knows a single lane runs the block (−2 % at C2, +1–1.5 % at C5
+    // and sustained against `lane == 0`, profiles/r02_elect_ab.txt)
+    if (j + S < je && elect_one()) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue_state(slot, j + S, true);
     }
