@@ -660,6 +660,26 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ri
       bulk_g2s(dst + SlotT::G, a.ug + o, kStateBlk * 16, bar);
     }
   };
+  // the row loop's refill of row jr: the same copies with running pointers
+  // (advanced by one row each iteration) instead of per-row 64-bit products
+  // (+1-2 % at C2, +1.5 % sustained, neutral at C5 burst;
+  // profiles/r02_runptr_ab.txt)
+  auto issue_row = [&](int s, int jr, const double2* csrc, const double2* xsrc, ptrdiff_t o) {
+    const uint32_t bar = bar0 + s * 8;
+    const uint32_t dst = smem_u32(ring + (size_t)s * SB);
+    const int rn = jr + 1 + R;
+    const bool st = (jr + 1 < je) && !(rn >= n && a.phys_hi);
+    mbar_expect_tx(bar, SlotT::BYTES - (st ? 0 : kStateBlk * 16));
+    HWG_CHK(jr >= 0 && jr < n && csrc == cblk + jr * crs && xsrc == xblk + rn * rs);
+    HWG_CHK(!st || in_reg(xsrc, a.x, rs, n, kStateBlk));
+    bulk_g2s(dst + SlotT::COEF, csrc, kCoefBlk * 16, bar);
+    if (st) bulk_g2s(dst + SlotT::XN, xsrc, kStateBlk * 16, bar);
+    if (SlotT::HAS_A) bulk_g2s(dst + SlotT::A, a.ua + o, kStateBlk * 16, bar);
+    if (SlotT::HAS_BG) {
+      bulk_g2s(dst + SlotT::B, a.ub + o, kStateBlk * 16, bar);
+      bulk_g2s(dst + SlotT::G, a.ug + o, kStateBlk * 16, bar);
+    }
+  };
   const int nq = live ? (je - jb < S ? je - jb : S) : 0;  // slots primed
   // ---- prologue, overlapping the previous stage's tail (programmatic launch)
   if (lane == 0 && live) {
@@ -762,6 +782,10 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ri
 #else
   constexpr int kUnroll = SCH == WENO5 ? 2 : 1;
 #endif
+  // running sources of the refill S rows ahead (issue_row)
+  const double2* iss_c = cblk + (ptrdiff_t)(jb + S) * crs;
+  const double2* iss_x = xblk + (ptrdiff_t)(jb + S + 1 + R) * rs;
+  ptrdiff_t iss_o = (ptrdiff_t)(jb + S) * rs + chunk * kStateBlk;
 #pragma unroll kUnroll
   for (int j = jb; j < je; ++j) {
     const unsigned char* sl = ring + (size_t)slot * SB;
@@ -945,8 +969,11 @@ __device__ __forceinline__ bool stage_body(const StageArgs& a, unsigned char* ri
     // and sustained against `lane == 0`, profiles/r02_elect_ab.txt)
     if (j + S < je && elect_one()) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_state(slot, j + S, true);
+      issue_row(slot, j + S, iss_c, iss_x, iss_o);
     }
+    iss_c += crs;
+    iss_x += rs;
+    iss_o += rs;
     if (++slot == S) { slot = 0; parity ^= 1u; }
   }
   if ((a.px.on_lo && jb == 0) | (a.px.on_hi && je == n))
